@@ -1,0 +1,145 @@
+/*
+ * spardec_b200.h — C ABI of the B200-native PillarAttn decode hot path.
+ *
+ * The reference (arXiv 2512.01278, `spardec`, /root/reference/pkg/src/spardec)
+ * is pure Python/numpy: it has NO native plugin or FFI.  Its drop-in boundary
+ * is the Python API; each entry point below replaces the arithmetic behind one
+ * reference function, and the Python host package (paper_2512_01278_b200)
+ * binds them with ctypes exactly where the reference calls that function:
+ *
+ *   sd_rope_kv_write      model.py:217-222 (_rotate) + model.py:271-287,326-331,
+ *                         372-374 (KV rows pushed into the per-layer buffer)
+ *   sd_attention          model.py:229-253 (_attend) as used by forward_full
+ *                         (model.py:318-334, verify / prefill, with score
+ *                         capture feeding selection.py:78-135) and by
+ *                         forward_sparse (model.py:360-380, critical U fresh U self)
+ *   sd_select_critical    engine.py:147-151 (_refresh_critical) =
+ *                         selection.py:207-218 (importance_from_log) +
+ *                         selection.py:167-183 (compute_budget) +
+ *                         selection.py:186-204 (select_critical_tokens)
+ *   sd_topk               selection.py:186-204 (select_critical_tokens)
+ *   sd_argmax_rows        model.py:388-390 (greedy_token)
+ *   sd_greedy_accept      engine.py:231-239 (verify_round accept loop + bonus)
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; every pointer is device memory unless
+ *     stated.  The library never allocates: buffers and workspaces are owned
+ *     by the caller (SURVEY.md §8b "Ownership").
+ *   - Every call is asynchronous on the caller's cudaStream_t (passed as void*).
+ *   - Return value: 0 = ok; < 0 = contract violation (message in
+ *     sd_last_error(), thread-local); > 0 = CUDA error code.  The Python shim
+ *     maps < 0 to ContractError and > 0 to RuntimeError (errors.py:8-37).
+ */
+#ifndef SPARDEC_B200_H
+#define SPARDEC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SD_ABI_VERSION 1
+
+#define SD_DTYPE_F32 0
+#define SD_DTYPE_BF16 1
+
+/* Fields of one attention work item (int32 record of SD_ITEM_FIELDS). */
+#define SD_ITEM_TABLE_ROW 0 /* block-table row of the request                      */
+#define SD_ITEM_Q_ROW0 1    /* first query row in q/out                             */
+#define SD_ITEM_NQ 2        /* query tokens in this item                            */
+#define SD_ITEM_QPOS0 3     /* absolute position of query token 0                   */
+#define SD_ITEM_CRIT_OFF 4  /* offset of this item's critical list in `crit`        */
+#define SD_ITEM_CRIT_LEN 5  /* number of critical positions (all < DENSE_LO)        */
+#define SD_ITEM_DENSE_LO 6  /* dense keys are [DENSE_LO, QPOS0 + NQ), causal        */
+#define SD_ITEM_ACC_ROW 7   /* first score-accumulator row, -1 = no score capture   */
+#define SD_ITEM_ACC_STEP 8  /* accumulator row step per query token (0 = sum rows)  */
+#define SD_ITEM_FIELDS 12
+
+/* Paged KV pool.  K and V: [layers][num_slots][kv_heads][head_dim] of dtype.
+ * Logical position p of table row r lives in slot
+ *   block_table[r * table_stride + (p >> page_shift)] << page_shift | (p & mask). */
+typedef struct sd_paged_kv {
+  void* k;
+  void* v;
+  int64_t layer_stride; /* elements between consecutive layers                 */
+  int64_t num_slots;
+  const int32_t* block_table;
+  int32_t table_stride; /* pages per table row                                  */
+  int32_t page_shift;   /* log2(tokens per page)                                */
+  int32_t kv_heads;
+  int32_t head_dim;
+  int32_t dtype; /* SD_DTYPE_*                                                    */
+  int32_t reserved;
+} sd_paged_kv;
+
+int32_t sd_abi_version(void);
+const char* sd_last_error(void);
+/* Number of kernels launched by this process through the library (evidence). */
+int64_t sd_launch_count(void);
+
+/* K5: RoPE (NeoX half split, base 1e4) of q and k at row_pos[r]; k and v are
+ * written into the pool at (row_table[r], row_pos[r]) of `layer`; rotated q is
+ * written to q_out [rows][q_heads][head_dim].  qkv row = [q | k | v]. */
+int sd_rope_kv_write(const void* qkv, int64_t qkv_row_stride, int32_t rows,
+                     const int32_t* row_table, const int32_t* row_pos,
+                     const sd_paged_kv* kv, int32_t layer, int32_t q_heads,
+                     void* q_out, void* stream);
+
+/* K1 + K2: grouped-query attention of every item's query rows over its keys
+ * (critical list, then dense causal range), two-phase exact softmax.
+ *   q, out   : [rows][q_heads][head_dim] of kv->dtype
+ *   lse      : [rows][q_heads] float or NULL
+ *   items    : device int32 [num_items][SD_ITEM_FIELDS]
+ *   crit     : device int32 critical positions (concatenated) or NULL
+ *   acc      : float score accumulators; row a has acc_row_stride floats; for
+ *              item query token t the row is ACC_ROW + t*ACC_STEP and
+ *              acc[row][pos] += sum over the group's q heads of exp(s - lse)
+ *   planted  : device int32 sorted positions receiving +planted_bonus, or NULL
+ *   max_keys, max_nq : host upper bounds over items (launch shaping)
+ *   workspace: device scratch (see sd_attention_workspace_bytes)
+ *   flags    : bit0 = force the generic (FFMA) kernel */
+int64_t sd_attention_workspace_bytes(int32_t num_items, int32_t max_keys, int32_t max_nq,
+                                     int32_t q_heads, const sd_paged_kv* kv);
+int sd_attention(const void* q, void* out, float* lse, const sd_paged_kv* kv, int32_t layer,
+                 const int32_t* items, int32_t num_items, int32_t max_keys, int32_t max_nq,
+                 const int32_t* crit, float* acc, int64_t acc_row_stride,
+                 const int32_t* planted, int32_t num_planted, float planted_bonus,
+                 int32_t q_heads, float scale, void* workspace, int64_t workspace_bytes,
+                 int32_t flags, void* stream);
+
+/* K3: per request r: importance[p] = sum_{t < n_rows[r]} acc[r][t][p] for
+ * p < kv_len[r]; budget = max(1, min(ceil(s*n - 1e-9), n)) (n = 0 -> 1);
+ * crit[r][:] = top-budget positions (value desc, ties to the lower index),
+ * ascending; crit_len[r] = min(budget, kv_len[r]).  importance may be NULL
+ * (then it is kept in `workspace`, num_requests * imp_stride floats). */
+int sd_select_critical(const float* acc, int64_t acc_req_stride, int64_t acc_row_stride,
+                       const int32_t* n_rows, const int32_t* kv_len, double sparsity,
+                       int32_t num_requests, float* importance, int64_t imp_stride,
+                       int32_t* crit, int64_t crit_stride, int32_t* crit_len,
+                       int32_t* budget_out, void* stream);
+
+/* Plain top-k (selection.py:186-204) over float32 (dtype 0) or float64
+ * (dtype 2) rows: values [num][stride], n[num], budget[num] -> out, out_len. */
+int sd_topk(const void* values, int32_t value_dtype, int64_t stride, const int32_t* n,
+            const int32_t* budget, int32_t num, int32_t* out, int64_t out_stride,
+            int32_t* out_len, void* stream);
+
+/* K4a: per-row argmax, ties to the lowest index.  logits [rows][row_stride]. */
+int sd_argmax_rows(const void* logits, int32_t dtype, int64_t row_stride, int32_t rows,
+                   int32_t vocab, int32_t* out, void* stream);
+
+/* K4b: per verify member m: rows [row0[m], row0[m]+nrows[m]) hold the targets
+ * of [pending, d_0 .. d_{n-2}]; tokens[] holds the verify INPUT tokens in the
+ * same rows.  accepted[m] = longest prefix i with tokens[row0+1+i] ==
+ * targets[row0+i]; bonus[m] = targets[row0 + accepted[m]]. */
+int sd_greedy_accept(const int32_t* targets, const int32_t* tokens, const int32_t* row0,
+                     const int32_t* nrows, int32_t num, int32_t* accepted, int32_t* bonus,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPARDEC_B200_H */

@@ -1,0 +1,63 @@
+// C-ABI surface: error state, launch accounting, attention dispatch.
+#include <atomic>
+#include <string>
+
+#include "common.cuh"
+
+namespace sd {
+
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int64_t generic_ws_bytes(int num_items, int max_keys, int max_rows, int kv_heads);
+int launch_attn_generic(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer,
+                        const int32_t* items, int num_items, int max_keys, int max_nq, const int32_t* crit,
+                        float* acc, int64_t acc_stride, const int32_t* planted, int n_planted, float bonus,
+                        int q_heads, float scale, void* ws, int64_t ws_bytes, cudaStream_t stream);
+bool mma_attn_supported(int dtype, int D, int rows);
+int launch_attn_mma(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer,
+                    const int32_t* items, int num_items, int max_keys, int max_nq, const int32_t* crit,
+                    float* acc, int64_t acc_stride, const int32_t* planted, int n_planted, float bonus,
+                    int q_heads, float scale, cudaStream_t stream, bool* handled);
+
+}  // namespace sd
+
+extern "C" int32_t sd_abi_version(void) { return SD_ABI_VERSION; }
+extern "C" const char* sd_last_error(void) { return sd::g_last_error.c_str(); }
+extern "C" int64_t sd_launch_count(void) { return sd::g_launches.load(); }
+
+extern "C" int64_t sd_attention_workspace_bytes(int32_t num_items, int32_t max_keys, int32_t max_nq,
+                                                int32_t q_heads, const sd_paged_kv* kv) {
+  if (kv == nullptr || kv->kv_heads <= 0) return 0;
+  const int G = q_heads / kv->kv_heads;
+  if (sd::mma_attn_supported(kv->dtype, kv->head_dim, max_nq * G)) return 0;
+  return sd::generic_ws_bytes(num_items, max_keys, max_nq * G, kv->kv_heads);
+}
+
+extern "C" int sd_attention(const void* q, void* out, float* lse, const sd_paged_kv* kv, int32_t layer,
+                            const int32_t* items, int32_t num_items, int32_t max_keys, int32_t max_nq,
+                            const int32_t* crit, float* acc, int64_t acc_row_stride, const int32_t* planted,
+                            int32_t num_planted, float planted_bonus, int32_t q_heads, float scale,
+                            void* workspace, int64_t workspace_bytes, int32_t flags, void* stream) {
+  SD_REQUIRE(kv != nullptr && q != nullptr && out != nullptr && items != nullptr, "sd_attention: null pointer");
+  SD_REQUIRE(kv->kv_heads > 0 && q_heads % kv->kv_heads == 0, "sd_attention: kv_heads must divide q_heads");
+  SD_REQUIRE(kv->dtype == SD_DTYPE_F32 || kv->dtype == SD_DTYPE_BF16, "sd_attention: unsupported dtype");
+  SD_REQUIRE(kv->page_shift >= 0 && kv->page_shift < 16, "sd_attention: bad page_shift");
+  SD_REQUIRE(max_nq >= 1 && max_keys >= 1, "sd_attention: max_nq and max_keys must be positive");
+  SD_REQUIRE(num_planted == 0 || planted != nullptr, "sd_attention: planted list missing");
+  if (num_items == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!(flags & 1)) {
+    bool handled = false;
+    const int rc = sd::launch_attn_mma(q, out, lse, kv, layer, items, num_items, max_keys, max_nq, crit, acc,
+                                       acc_row_stride, planted, num_planted, planted_bonus, q_heads, scale, s,
+                                       &handled);
+    if (handled || rc != 0) return rc;
+  }
+  return sd::launch_attn_generic(q, out, lse, kv, layer, items, num_items, max_keys, max_nq, crit, acc,
+                                 acc_row_stride, planted, num_planted, planted_bonus, q_heads, scale, workspace,
+                                 workspace_bytes, s);
+}

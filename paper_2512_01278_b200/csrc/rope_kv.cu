@@ -1,0 +1,72 @@
+// K5: RoPE epilogue of the QKV projection + paged KV append.
+// Restates model.py:212-222 (_rotate: NeoX half split, inv_freq = 1e4^(-2i/d),
+// angle at the ABSOLUTE position) and the K/V push of model.py:284-287,
+// 326-331, 372-374.  K is stored post-RoPE (drafts gather rotated keys);
+// rows go straight into their paged slot (no per-forward buffer copy,
+// model.py:271-287's _LayerBuffer is eliminated).
+#include "common.cuh"
+
+namespace sd {
+
+template <typename T>
+__global__ void __launch_bounds__(128) rope_kv_kernel(const T* __restrict__ qkv, int64_t row_stride,
+                                                      const int32_t* __restrict__ row_table,
+                                                      const int32_t* __restrict__ row_pos, PagedKv kv,
+                                                      int layer, int q_heads, T* __restrict__ q_out) {
+  const int r = blockIdx.x;
+  const int D = kv.head_dim, half = D / 2, Hkv = kv.kv_heads;
+  const int pos = row_pos[r];
+  const int64_t slot = kv.slot_of(row_table[r], pos);
+  const T* x = qkv + (int64_t)r * row_stride;
+  T* K = static_cast<T*>(const_cast<void*>(kv.k)) + (int64_t)layer * kv.layer_stride;
+  T* V = static_cast<T*>(const_cast<void*>(kv.v)) + (int64_t)layer * kv.layer_stride;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    // angle in double exactly as numpy: position * 10000 ** (-(2i)/d)
+    const double inv = pow(10000.0, -static_cast<double>(2 * i) / static_cast<double>(D));
+    double s, c;
+    sincos(static_cast<double>(pos) * inv, &s, &c);
+    for (int hq = 0; hq < q_heads + Hkv; ++hq) {
+      const T* src = x + hq * D;
+      float lo, hi;
+      if constexpr (sizeof(T) == 4) {  // parity mode: rotate in double, round once
+        const double a = to_f(src[i]), b = to_f(src[i + half]);
+        lo = static_cast<float>(a * c - b * s);
+        hi = static_cast<float>(a * s + b * c);
+      } else {
+        const float a = to_f(src[i]), b = to_f(src[i + half]);
+        const float cf = static_cast<float>(c), sf = static_cast<float>(s);
+        lo = a * cf - b * sf;
+        hi = a * sf + b * cf;
+      }
+      T* dst = hq < q_heads ? q_out + ((int64_t)r * q_heads + hq) * D : K + kv.row_off(slot, hq - q_heads);
+      dst[i] = from_f<T>(lo);
+      dst[i + half] = from_f<T>(hi);
+    }
+  }
+  const T* vsrc = x + (q_heads + Hkv) * D;
+  T* vdst = V + kv.row_off(slot, 0);
+  for (int j = threadIdx.x; j < Hkv * D; j += blockDim.x) vdst[j] = vsrc[j];
+}
+
+}  // namespace sd
+
+extern "C" int sd_rope_kv_write(const void* qkv, int64_t qkv_row_stride, int32_t rows,
+                                const int32_t* row_table, const int32_t* row_pos, const sd_paged_kv* kv,
+                                int32_t layer, int32_t q_heads, void* q_out, void* stream) {
+  SD_REQUIRE(kv != nullptr && qkv != nullptr && q_out != nullptr, "sd_rope_kv_write: null pointer");
+  SD_REQUIRE(rows >= 0, "sd_rope_kv_write: negative row count");
+  SD_REQUIRE(kv->head_dim % 2 == 0, "sd_rope_kv_write: head_dim must be even");
+  SD_REQUIRE(q_heads % kv->kv_heads == 0, "sd_rope_kv_write: kv_heads must divide q_heads");
+  if (rows == 0) return 0;
+  sd::PagedKv p = sd::make_paged(kv);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (kv->dtype == SD_DTYPE_F32)
+    sd::rope_kv_kernel<float><<<rows, 128, 0, s>>>(static_cast<const float*>(qkv), qkv_row_stride, row_table,
+                                                  row_pos, p, layer, q_heads, static_cast<float*>(q_out));
+  else
+    sd::rope_kv_kernel<__nv_bfloat16><<<rows, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(qkv),
+                                                          qkv_row_stride, row_table, row_pos, p, layer,
+                                                          q_heads, static_cast<__nv_bfloat16*>(q_out));
+  sd::count_launch();
+  SD_CUDA_RETURN();
+}

@@ -1,0 +1,102 @@
+"""Typed Python entry points over the C ABI (one call = one stream-ordered
+launch on the current CUDA stream).  Shapes are validated here, mirroring the
+reference's host-side contract checks, before anything is launched."""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native as N
+from .errors import ContractError
+
+
+def rope_kv_write(qkv: torch.Tensor, row_table: torch.Tensor, row_pos: torch.Tensor, pool, layer: int,
+                  q_heads: int, q_out: torch.Tensor) -> None:
+    """K5: RoPE q/k at row_pos, write k/v into the paged pool, rotated q to q_out."""
+    rows = qkv.shape[0]
+    if rows == 0:
+        return
+    N.require_cuda(qkv, "qkv")
+    if qkv.stride(1) != 1 or q_out.dtype != pool.dtype or qkv.dtype != pool.dtype:
+        raise ContractError("rope_kv_write: qkv/q_out must match the pool dtype with unit inner stride")
+    desc = pool.desc()
+    N.check(N.lib().sd_rope_kv_write(qkv.data_ptr(), qkv.stride(0), rows, row_table.data_ptr(),
+                                     row_pos.data_ptr(), ctypes.byref(desc), layer, q_heads,
+                                     q_out.data_ptr(), N.stream_handle()), "sd_rope_kv_write")
+
+
+def attention(q: torch.Tensor, out: torch.Tensor, pool, layer: int, items: torch.Tensor, num_items: int,
+              max_keys: int, max_nq: int, q_heads: int, *, crit: torch.Tensor | None = None,
+              lse: torch.Tensor | None = None, acc: torch.Tensor | None = None, acc_row_stride: int = 0,
+              planted: torch.Tensor | None = None, planted_bonus: float = 0.0, scale: float | None = None,
+              workspace: torch.Tensor | None = None, force_generic: bool = False) -> None:
+    """K1/K2: paged GQA attention over the work items (see spardec_b200.h)."""
+    if num_items == 0:
+        return
+    desc = pool.desc()
+    lib = N.lib()
+    need = lib.sd_attention_workspace_bytes(num_items, max_keys, max_nq, q_heads, ctypes.byref(desc))
+    if force_generic:
+        G = q_heads // pool.kv_heads
+        need = num_items * pool.kv_heads * (max_nq * G * max_keys + 2 * max_keys) * 4
+    if need > 0 and (workspace is None or workspace.numel() * workspace.element_size() < need):
+        workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    if scale is None:
+        scale = 1.0 / (pool.head_dim ** 0.5)
+    n_planted = 0 if planted is None else planted.numel()
+    N.check(lib.sd_attention(q.data_ptr(), out.data_ptr(), N.ptr(lse), ctypes.byref(desc), layer,
+                             items.data_ptr(), num_items, max_keys, max_nq, N.ptr(crit), N.ptr(acc),
+                             acc_row_stride, N.ptr(planted), n_planted, planted_bonus, q_heads, scale,
+                             N.ptr(workspace), ws_bytes, 1 if force_generic else 0, N.stream_handle()),
+            "sd_attention")
+
+
+def select_critical(acc: torch.Tensor, acc_req_stride: int, acc_row_stride: int, n_rows: torch.Tensor,
+                    kv_len: torch.Tensor, sparsity: float, num: int, importance: torch.Tensor,
+                    crit: torch.Tensor, crit_len: torch.Tensor, budget: torch.Tensor | None = None) -> None:
+    """K3: importance = sum of the surviving score rows; budget; tie-exact top-k."""
+    if num == 0:
+        return
+    N.check(N.lib().sd_select_critical(acc.data_ptr(), acc_req_stride, acc_row_stride, n_rows.data_ptr(),
+                                       kv_len.data_ptr(), float(sparsity), num, importance.data_ptr(),
+                                       importance.stride(0), crit.data_ptr(), crit.stride(0),
+                                       crit_len.data_ptr(), N.ptr(budget), N.stream_handle()),
+            "sd_select_critical")
+
+
+def topk(values: torch.Tensor, n: torch.Tensor, budget: torch.Tensor, out: torch.Tensor,
+         out_len: torch.Tensor) -> None:
+    """Batched tie-exact top-k over rows of float32/float64 values."""
+    if values.dtype == torch.float32:
+        code = 0
+    elif values.dtype == torch.float64:
+        code = 2
+    else:
+        raise ContractError("topk values must be float32 or float64")
+    N.check(N.lib().sd_topk(values.data_ptr(), code, values.stride(0), n.data_ptr(), budget.data_ptr(),
+                            values.shape[0], out.data_ptr(), out.stride(0), out_len.data_ptr(),
+                            N.stream_handle()), "sd_topk")
+
+
+def argmax_rows(logits: torch.Tensor, out: torch.Tensor) -> None:
+    """K4a: per-row argmax with ties to the lowest id."""
+    rows, vocab = logits.shape
+    if logits.stride(1) != 1:
+        raise ContractError("argmax_rows: logits rows must be contiguous")
+    N.check(N.lib().sd_argmax_rows(logits.data_ptr(), N.dtype_code(logits.dtype), logits.stride(0), rows,
+                                   vocab, out.data_ptr(), N.stream_handle()), "sd_argmax_rows")
+
+
+def greedy_accept(targets: torch.Tensor, tokens: torch.Tensor, row0: torch.Tensor, nrows: torch.Tensor,
+                  accepted: torch.Tensor, bonus: torch.Tensor) -> None:
+    """K4b: longest accepted draft prefix and the bonus token per verify member."""
+    N.check(N.lib().sd_greedy_accept(targets.data_ptr(), tokens.data_ptr(), row0.data_ptr(), nrows.data_ptr(),
+                                     row0.numel(), accepted.data_ptr(), bonus.data_ptr(), N.stream_handle()),
+            "sd_greedy_accept")
+
+
+def launch_count() -> int:
+    return int(N.lib().sd_launch_count())

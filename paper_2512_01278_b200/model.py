@@ -1,0 +1,435 @@
+"""Toy decoder (the reference's oracle architecture) on the B200, and the
+drop-in attention operators.
+
+Same public names as the reference model.py: ``ModelConfig``, ``ToyModel``,
+``init_model``, ``plant_attention_concentration``, ``KVEntry``, ``KvCache``,
+``forward_full``, ``forward_sparse``, ``greedy_token``.
+
+Architecture (model.py:1-17): pre-norm GQA blocks, RMSNorm without gain
+(model.py:225), NeoX RoPE base 1e4 (model.py:212-222), tanh MLP of width 2h
+(model.py:181,336), tied embedding / LM head (model.py:339), 1/sqrt(d) logit
+scale (model.py:245), q head h -> kv head h // G (model.py:244).
+
+Linear layers run on torch.matmul (cuBLAS; TF32 disabled in fp32 parity
+mode).  RoPE + KV append (K5) and attention (K1/K2) are the in-tree sm_100a
+kernels; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import kernels as K
+from .errors import ConfigurationError, ContractError
+from .paged import PagedKvPool
+from .selection import AttentionScoreLog, CriticalTokenSet
+
+INIT_SCALE = 0.08   # model.py:31
+RMS_EPS = 1e-6      # model.py:32
+ROPE_BASE = 10000.0  # model.py:33
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """Shape and seed (model.py:36-74). hidden_dim is pinned to Hq * d."""
+
+    num_layers: int
+    num_q_heads: int
+    num_kv_heads: int
+    head_dim: int
+    vocab_size: int
+    seed: int = 0
+    hidden_dim: int | None = None
+
+    def __post_init__(self) -> None:
+        if min(self.num_layers, self.num_q_heads, self.num_kv_heads, self.head_dim) < 1:
+            raise ConfigurationError("model dimensions must be at least 1")
+        if self.vocab_size < 2:
+            raise ConfigurationError("vocab_size must be at least 2")
+        if self.num_q_heads % self.num_kv_heads:
+            raise ConfigurationError(f"num_kv_heads={self.num_kv_heads} must divide num_q_heads={self.num_q_heads}")
+        if self.head_dim % 2:
+            raise ConfigurationError("head_dim must be even for rotary mixing")
+        want = self.num_q_heads * self.head_dim
+        if self.hidden_dim is None:
+            object.__setattr__(self, "hidden_dim", want)
+        elif self.hidden_dim != want:
+            raise ConfigurationError(f"hidden_dim must equal num_q_heads * head_dim = {want}")
+
+    @property
+    def group_size(self) -> int:
+        return self.num_q_heads // self.num_kv_heads
+
+
+@dataclass(frozen=True)
+class PlantedConcentration:
+    """+bonus on listed positions for every layer/head/query (model.py:87-97)."""
+
+    positions: tuple
+    bonus: float = 2000.0
+
+
+@dataclass(frozen=True)
+class LayerWeights:
+    """Views of one layer's matrices, (in, out) layout as the reference."""
+
+    mlp_in: torch.Tensor
+    mlp_out: torch.Tensor
+    wk: torch.Tensor
+    wo: torch.Tensor
+    wq: torch.Tensor
+    wv: torch.Tensor
+
+
+class ToyModel:
+    """Device-resident weights.  ``w_qkv[l]`` = [wq | wk | wv] (h, (Hq+2Hkv)d)
+    so one GEMM feeds the RoPE/KV-append kernel."""
+
+    def __init__(self, config: ModelConfig, embedding: torch.Tensor, w_qkv, wo, mlp_in, mlp_out,
+                 planted: PlantedConcentration | None = None):
+        self.config = config
+        self.embedding = embedding
+        self.w_qkv = list(w_qkv)
+        self.wo = list(wo)
+        self.mlp_in = list(mlp_in)
+        self.mlp_out = list(mlp_out)
+        self.planted = planted
+        self.dtype = embedding.dtype
+        self.device = embedding.device
+        self.planted_dev = None
+        if planted is not None and planted.positions:
+            self.planted_dev = torch.tensor(planted.positions, dtype=torch.int32, device=self.device)
+
+    @property
+    def layers(self) -> tuple:
+        c = self.config
+        qd, kd = c.num_q_heads * c.head_dim, c.num_kv_heads * c.head_dim
+        return tuple(
+            LayerWeights(mlp_in=self.mlp_in[l], mlp_out=self.mlp_out[l], wk=w[:, qd:qd + kd], wo=self.wo[l],
+                         wq=w[:, :qd], wv=w[:, qd + kd:])
+            for l, w in enumerate(self.w_qkv)
+        )
+
+    @property
+    def planted_bonus(self) -> float:
+        return 0.0 if self.planted is None else float(self.planted.bonus)
+
+    def with_planted(self, planted: PlantedConcentration | None) -> "ToyModel":
+        return ToyModel(self.config, self.embedding, self.w_qkv, self.wo, self.mlp_in, self.mlp_out, planted)
+
+
+def init_model(config: ModelConfig, dtype: torch.dtype = torch.float32, device="cuda",
+               fast_init: bool = False) -> ToyModel:
+    """Weights ~ N(0, 0.08) drawn exactly like the reference (model.py:171-195):
+    SFC64(seed), embedding first, then per layer mlp_in, mlp_out, wk, wo, wq,
+    wv, each row-major.  Every matrix is converted and uploaded as soon as it
+    is drawn so host memory stays bounded.
+
+    ``fast_init=True`` draws the same shapes from a seeded on-device torch
+    generator instead (benchmark-scale models: identical architecture, not
+    bit-identical values)."""
+    dev = torch.device(device)
+    h = config.hidden_dim
+    kvw = config.num_kv_heads * config.head_dim
+    shapes = [("mlp_in", (h, 2 * h)), ("mlp_out", (2 * h, h)), ("wk", (h, kvw)), ("wo", (h, h)),
+              ("wq", (h, h)), ("wv", (h, kvw))]
+    if fast_init:
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(config.seed)
+
+        def draw(shape):
+            return (torch.randn(shape, generator=gen, device=dev, dtype=torch.float32) * INIT_SCALE).to(dtype)
+    else:
+        rng = np.random.Generator(np.random.SFC64(config.seed))
+
+        def draw(shape):
+            return torch.from_numpy(rng.normal(0.0, INIT_SCALE, shape)).to(device=dev, dtype=dtype)
+
+    emb = draw((config.vocab_size, h))
+    w_qkv, wo, mlp_in, mlp_out = [], [], [], []
+    for _ in range(config.num_layers):
+        m = {name: draw(shape) for name, shape in shapes}
+        w_qkv.append(torch.cat([m["wq"], m["wk"], m["wv"]], dim=1).contiguous())
+        wo.append(m["wo"])
+        mlp_in.append(m["mlp_in"])
+        mlp_out.append(m["mlp_out"])
+        del m
+    return ToyModel(config, emb, w_qkv, wo, mlp_in, mlp_out)
+
+
+def plant_attention_concentration(model: ToyModel, positions: Sequence[int], bonus: float = 2000.0) -> ToyModel:
+    """model.py:198-209 (weights are shared, not copied)."""
+    pos = tuple(sorted(int(p) for p in positions))
+    if len(pos) != len(set(pos)) or (pos and pos[0] < 0):
+        raise ContractError("planted positions must be unique and non-negative")
+    return model.with_planted(PlantedConcentration(positions=pos, bonus=bonus))
+
+
+# ---------------------------------------------------------------------------------
+# batched forward core (shared by the drop-in operators and the batched decoder)
+# ---------------------------------------------------------------------------------
+
+
+def rmsnorm(x: torch.Tensor) -> torch.Tensor:
+    """model.py:225-226 (fp32 statistics)."""
+    return x * torch.rsqrt(torch.mean(x * x, dim=-1, keepdim=True) + RMS_EPS)
+
+
+def _mm(a: torch.Tensor, b: torch.Tensor, out_f32: bool) -> torch.Tensor:
+    if a.dtype == torch.float32 or not out_f32:
+        return torch.mm(a, b)
+    return torch.mm(a, b, out_dtype=torch.float32)
+
+
+@dataclass
+class AttnLaunch:
+    """One sd_attention launch over a homogeneous group of work items."""
+
+    items: torch.Tensor           # device int32 [n, ITEM_FIELDS]
+    num_items: int
+    max_keys: int
+    max_nq: int
+    crit: torch.Tensor | None = None
+    acc: torch.Tensor | None = None
+    acc_row_stride: int = 0
+    timer: object | None = None   # optional callable(start: bool) for per-launch timing
+
+
+def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_table: torch.Tensor,
+                 row_pos: torch.Tensor, launches: Sequence[AttnLaunch], lse_out: torch.Tensor | None = None,
+                 force_generic: bool = False) -> torch.Tensor:
+    """Run every layer for R rows at once and return the final hidden (R, h) fp32.
+
+    Row r is token ``tokens[r]`` at absolute position ``row_pos[r]`` of the
+    request mapped to block-table row ``row_table[r]``; its K/V are written
+    into the pool before attention (K5), so a verify window attends causally to
+    its own earlier rows exactly like the reference's token-at-a-time loop
+    (model.py:318-340), and a draft row attends to critical U fresh U self
+    (model.py:360-380)."""
+    c = model.config
+    R = tokens.shape[0]
+    Hq, d = c.num_q_heads, c.head_dim
+    dt = model.dtype
+    x = model.embedding.index_select(0, tokens.long()).float()
+    q_buf = torch.empty(R, Hq, d, dtype=dt, device=model.device)
+    ctx = torch.empty(R, Hq, d, dtype=dt, device=model.device)
+    for l in range(c.num_layers):
+        hn = rmsnorm(x).to(dt)
+        qkv = torch.mm(hn, model.w_qkv[l])
+        K.rope_kv_write(qkv, row_table, row_pos, pool, l, Hq, q_buf)
+        for ln in launches:
+            if ln.timer is not None:
+                ln.timer(True)
+            K.attention(q_buf, ctx, pool, l, ln.items, ln.num_items, ln.max_keys, ln.max_nq, Hq,
+                        crit=ln.crit, lse=None if lse_out is None else lse_out[l], acc=ln.acc,
+                        acc_row_stride=ln.acc_row_stride, planted=model.planted_dev,
+                        planted_bonus=model.planted_bonus, force_generic=force_generic)
+            if ln.timer is not None:
+                ln.timer(False)
+        x = x + _mm(ctx.view(R, Hq * d), model.wo[l], True)
+        hm = torch.tanh(_mm(rmsnorm(x).to(dt), model.mlp_in[l], True)).to(dt)
+        x = x + _mm(hm, model.mlp_out[l], True)
+    return x
+
+
+def lm_head(model: ToyModel, x: torch.Tensor) -> torch.Tensor:
+    """logits = E . rmsnorm(x) (model.py:339), fp32 output."""
+    return _mm(rmsnorm(x).to(model.dtype), model.embedding.t(), True)
+
+
+def make_items(rows: list[tuple], device) -> torch.Tensor:
+    """rows of (table_row, q_row0, nq, qpos0, crit_off, crit_len, dense_lo, acc_row, acc_step)."""
+    arr = np.zeros((max(1, len(rows)), N.ITEM_FIELDS), dtype=np.int32)
+    for i, r in enumerate(rows):
+        arr[i, :9] = r
+    return torch.from_numpy(arr).to(device, non_blocking=False)
+
+
+# ---------------------------------------------------------------------------------
+# drop-in per-request KV cache and operators
+# ---------------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class KVEntry:
+    """Post-rotary K/V of one token: (layers, kv_heads, head_dim) (model.py:108-119)."""
+
+    k: torch.Tensor
+    v: torch.Tensor
+
+    def validate(self) -> None:
+        if self.k.shape != self.v.shape or self.k.dim() != 3:
+            raise ContractError("KV entry arrays must share a (layers, heads, dim) shape")
+        if not (bool(torch.isfinite(self.k).all()) and bool(torch.isfinite(self.v).all())):
+            raise ContractError("KV entry contains non-finite values")
+
+
+class KvCache:
+    """Per-request KV store (model.py:122-168) backed by a one-row device
+    paged pool.  ``len`` is the committed length; slots past it hold
+    provisional rows written by forwards and are never read as committed."""
+
+    PAGE = 16
+
+    def __init__(self, config: ModelConfig, capacity: int = 16, dtype: torch.dtype = torch.float32,
+                 device="cuda"):
+        self.config = config
+        self.dtype = dtype
+        self.device = torch.device(device)
+        self._n = 0
+        self._pool = self._new_pool(max(capacity, 1))
+
+    def _new_pool(self, capacity: int) -> PagedKvPool:
+        pages = -(-capacity // self.PAGE)
+        c = self.config
+        pool = PagedKvPool(c.num_layers, c.num_kv_heads, c.head_dim, pages, self.PAGE, 1, pages, self.dtype,
+                           self.device)
+        pool.ensure_tokens(0, pages * self.PAGE)
+        pool.sync_table()
+        return pool
+
+    @property
+    def pool(self) -> PagedKvPool:
+        return self._pool
+
+    @property
+    def capacity(self) -> int:
+        return self._pool.num_pages * self.PAGE
+
+    def __len__(self) -> int:
+        return self._n
+
+    def ensure_capacity(self, need: int) -> None:
+        if need <= self.capacity:
+            return
+        fresh = self._new_pool(max(need, 2 * self.capacity))
+        fresh.k[:, : self.capacity] = self._pool.k
+        fresh.v[:, : self.capacity] = self._pool.v
+        self._pool = fresh
+
+    def append(self, entry: KVEntry) -> None:
+        self.extend([entry])
+
+    def extend(self, entries: Sequence[KVEntry]) -> None:
+        if not entries:
+            return
+        self.ensure_capacity(self._n + len(entries))
+        k = torch.stack([e.k for e in entries])
+        v = torch.stack([e.v for e in entries])
+        self._pool.write(0, range(self._n, self._n + len(entries)), k, v)
+        self._n += len(entries)
+
+    def truncate(self, n: int) -> None:
+        if not 0 <= n <= self._n:
+            raise ContractError("truncate target out of range")
+        self._n = n
+
+    def keys(self, layer: int) -> torch.Tensor:
+        return self._pool.k[layer, : self._n]
+
+    def values(self, layer: int) -> torch.Tensor:
+        return self._pool.v[layer, : self._n]
+
+    def gather(self, layer: int, positions) -> tuple[torch.Tensor, torch.Tensor]:
+        idx = torch.as_tensor(np.asarray(positions, dtype=np.int64), device=self.device)
+        return self._pool.k[layer, idx], self._pool.v[layer, idx]
+
+
+def _check_tokens(config: ModelConfig, tokens: Sequence[int]) -> None:
+    for t in tokens:
+        if not 0 <= int(t) < config.vocab_size:
+            raise ContractError(f"token id {t} outside vocab of {config.vocab_size}")
+
+
+def _require_cache_dtype(model: ToyModel, cache: KvCache) -> None:
+    if cache.dtype != model.dtype:
+        raise ContractError(f"cache dtype {cache.dtype} != model dtype {model.dtype}")
+
+
+def forward_full(model: ToyModel, committed_kv: KvCache, new_tokens: Sequence[int], capture_scores: bool = True):
+    """Verify / prefill forward (model.py:290-342).
+
+    Returns ``(logits (n, V) fp32, [KVEntry] * n, AttentionScoreLog)``.  The
+    cache's committed length is unchanged; the new tokens' K/V come back as
+    entries.  The score log carries the PillarAttn accumulator
+    acc[q][pos] = sum_{layer, head} exp(logit - lse) and the per-(layer, query,
+    head) lse, i.e. everything importance_from_log needs (selection.py:207-218)
+    without materialising logits."""
+    cfg = model.config
+    toks = [int(t) for t in new_tokens]
+    if not toks:
+        raise ContractError("forward_full needs at least one token")
+    _check_tokens(cfg, toks)
+    _require_cache_dtype(model, committed_kv)
+    n0, n = len(committed_kv), len(toks)
+    committed_kv.ensure_capacity(n0 + n)
+    pool = committed_kv.pool
+    dev = model.device
+    acc = torch.zeros(n, n0 + n, dtype=torch.float32, device=dev) if capture_scores else None
+    lse = torch.empty(cfg.num_layers, n, cfg.num_q_heads, dtype=torch.float32, device=dev) if capture_scores else None
+    items = make_items([(0, 0, n, n0, 0, 0, 0, 0 if capture_scores else -1, 1)], dev)
+    launch = AttnLaunch(items, 1, n0 + n, n, acc=acc, acc_row_stride=n0 + n)
+    tok = torch.tensor(toks, dtype=torch.int32, device=dev)
+    rt = torch.zeros(n, dtype=torch.int32, device=dev)
+    rp = torch.arange(n0, n0 + n, dtype=torch.int32, device=dev)
+    x = forward_rows(model, pool, tok, rt, rp, [launch], lse_out=lse)
+    logits = lm_head(model, x)
+    ks, vs = pool.read(0, range(n0, n0 + n))
+    entries = [KVEntry(k=ks[j].clone(), v=vs[j].clone()) for j in range(n)]
+    log = AttentionScoreLog(cfg.num_q_heads, cfg.num_kv_heads, cfg.num_layers, n0, acc, lse)
+    return logits, entries, log
+
+
+def forward_sparse(model: ToyModel, committed_kv: KvCache, critical: CriticalTokenSet,
+                   fresh_kv: Sequence[KVEntry], new_token: int):
+    """Draft forward (model.py:345-385): the token at n0 + len(fresh) attends to
+    the critical positions (< n0), every fresh entry and itself."""
+    cfg = model.config
+    _check_tokens(cfg, [new_token])
+    _require_cache_dtype(model, committed_kv)
+    n0 = len(committed_kv)
+    nf = len(fresh_kv)
+    pos = n0 + nf
+    crit = critical.device_positions(model.device)
+    if len(critical) and int(critical.positions[-1]) >= n0:
+        raise ContractError("critical positions must lie inside the committed cache")
+    committed_kv.ensure_capacity(pos + 1)
+    pool = committed_kv.pool
+    if nf:
+        pool.write(0, range(n0, pos), torch.stack([e.k for e in fresh_kv]), torch.stack([e.v for e in fresh_kv]))
+    dev = model.device
+    items = make_items([(0, 0, 1, pos, 0, len(critical), n0, -1, 0)], dev)
+    launch = AttnLaunch(items, 1, len(critical) + nf + 1, 1, crit=crit)
+    tok = torch.tensor([int(new_token)], dtype=torch.int32, device=dev)
+    rt = torch.zeros(1, dtype=torch.int32, device=dev)
+    rp = torch.tensor([pos], dtype=torch.int32, device=dev)
+    x = forward_rows(model, pool, tok, rt, rp, [launch])
+    logits = lm_head(model, x)[0]
+    ks, vs = pool.read(0, [pos])
+    return logits, KVEntry(k=ks[0].clone(), v=vs[0].clone())
+
+
+def greedy_token(logits) -> int:
+    """Argmax with ties to the lowest token id (model.py:388-390), on device."""
+    t = logits if isinstance(logits, torch.Tensor) else torch.as_tensor(np.asarray(logits))
+    if not t.is_cuda:
+        t = t.cuda()
+    if t.dtype not in (torch.float32, torch.bfloat16):
+        t = t.float()
+    t = t.reshape(1, -1).contiguous()
+    out = torch.empty(1, dtype=torch.int32, device=t.device)
+    K.argmax_rows(t, out)
+    return int(out.item())
+
+
+def greedy_tokens(logits: torch.Tensor) -> torch.Tensor:
+    """Row-wise greedy_token on device (int32 [rows])."""
+    out = torch.empty(logits.shape[0], dtype=torch.int32, device=logits.device)
+    K.argmax_rows(logits.contiguous(), out)
+    return out

@@ -1,0 +1,123 @@
+"""Device paged KV pool: the HBM layout every hot-path kernel reads.
+
+Layout:
+    K, V : [layers][num_pages * page_size][kv_heads][head_dim]   (bf16 / fp32)
+    table: [table_rows][pages_per_row] int32 physical page ids
+A token's K row for one kv head is head_dim contiguous elements (256 B at
+d=128 bf16), a token's row across heads is contiguous (2 KB at Hkv=8), and a
+page of 16 tokens is 32 KB contiguous per layer, so dense verify reads stream
+and sparse draft gathers move whole 16-byte-aligned rows.
+
+Logical page accounting stays one token per page exactly as the reference
+(kvpool.py:1-8); physical pages group ``page_size`` tokens.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ContractError, ImpossibleRequestError
+
+
+class PagedKvPool:
+    def __init__(self, layers: int, kv_heads: int, head_dim: int, num_pages: int, page_size: int,
+                 table_rows: int, pages_per_row: int, dtype: torch.dtype, device="cuda"):
+        if page_size < 1 or page_size & (page_size - 1):
+            raise ContractError("page_size must be a power of two")
+        if num_pages < 1 or table_rows < 1 or pages_per_row < 1:
+            raise ContractError("pool dimensions must be positive")
+        self.layers, self.kv_heads, self.head_dim = layers, kv_heads, head_dim
+        self.page_size = page_size
+        self.page_shift = page_size.bit_length() - 1
+        self.num_pages = num_pages
+        self.dtype = dtype
+        self.device = torch.device(device)
+        slots = num_pages * page_size
+        self.k = torch.zeros(layers, slots, kv_heads, head_dim, dtype=dtype, device=self.device)
+        self.v = torch.zeros_like(self.k)
+        self.table = torch.zeros(table_rows, pages_per_row, dtype=torch.int32, device=self.device)
+        self._table_host = np.zeros((table_rows, pages_per_row), dtype=np.int32)
+        self._dirty: set[int] = set()
+        self._free = list(range(num_pages - 1, -1, -1))
+        self._rows: dict[int, list[int]] = {}
+        self._desc = None
+
+    # -- descriptor ------------------------------------------------------------------
+    def desc(self) -> N.PagedKvDesc:
+        if self._desc is None:
+            d = N.PagedKvDesc()
+            d.k = self.k.data_ptr()
+            d.v = self.v.data_ptr()
+            d.layer_stride = self.k.stride(0)
+            d.num_slots = self.k.shape[1]
+            d.block_table = self.table.data_ptr()
+            d.table_stride = self.table.stride(0)
+            d.page_shift = self.page_shift
+            d.kv_heads = self.kv_heads
+            d.head_dim = self.head_dim
+            d.dtype = N.dtype_code(self.dtype)
+            self._desc = d
+        return self._desc
+
+    # -- page mapping ----------------------------------------------------------------
+    @property
+    def free_pages(self) -> int:
+        return len(self._free)
+
+    @property
+    def pages_per_row(self) -> int:
+        return self.table.shape[1]
+
+    def pages_of_row(self, row: int) -> list[int]:
+        return list(self._rows.get(row, []))
+
+    def ensure_tokens(self, row: int, tokens: int) -> None:
+        """Map enough physical pages for logical positions [0, tokens) of ``row``."""
+        need = -(-tokens // self.page_size)
+        if need > self.pages_per_row:
+            raise ImpossibleRequestError(f"row {row} needs {need} pages > {self.pages_per_row} per row")
+        pages = self._rows.setdefault(row, [])
+        if need - len(pages) > len(self._free):
+            raise ImpossibleRequestError("device KV pool exhausted")
+        while len(pages) < need:
+            p = self._free.pop()
+            self._table_host[row, len(pages)] = p
+            pages.append(p)
+            self._dirty.add(row)
+
+    def release_row(self, row: int) -> None:
+        for p in reversed(self._rows.pop(row, [])):
+            self._free.append(p)
+
+    def sync_table(self) -> None:
+        """Upload dirty block-table rows (host -> device, stream ordered)."""
+        if not self._dirty:
+            return
+        rows = sorted(self._dirty)
+        self._dirty.clear()
+        if len(rows) > 8:
+            self.table.copy_(torch.from_numpy(self._table_host), non_blocking=False)
+            return
+        for r in rows:
+            self.table[r].copy_(torch.from_numpy(self._table_host[r]))
+
+    # -- host-side views (tests / drop-in KvCache) -------------------------------------
+    def slots(self, row: int, positions) -> torch.Tensor:
+        pos = torch.as_tensor(np.asarray(positions, dtype=np.int64))
+        pages = torch.as_tensor(self._table_host[row]).long()[pos >> self.page_shift]
+        return (pages << self.page_shift) | (pos & (self.page_size - 1))
+
+    def read(self, row: int, positions) -> tuple[torch.Tensor, torch.Tensor]:
+        """K, V of ``positions``: (n, layers, kv_heads, head_dim)."""
+        s = self.slots(row, positions).to(self.device)
+        return self.k[:, s].transpose(0, 1), self.v[:, s].transpose(0, 1)
+
+    def write(self, row: int, positions, k: torch.Tensor, v: torch.Tensor) -> None:
+        """Store (n, layers, kv_heads, head_dim) rows at ``positions``."""
+        s = self.slots(row, positions).to(self.device)
+        self.k[:, s] = k.transpose(0, 1).to(self.dtype)
+        self.v[:, s] = v.transpose(0, 1).to(self.dtype)

@@ -1,0 +1,280 @@
+"""Kernel-level parity on the B200 (calls go through the C ABI).
+
+Oracles: oracle/pillar_oracle.attend_one (fp64 restatement of model.py:229-253,
+pinned to the reference) for attention outputs / lse; the reference's own
+golden top-k / budget known answers; numpy for argmax / accept.
+Tolerances (north_star): attention 1e-4 in fp32 mode, 2e-2 max-abs in bf16.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import pillar_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2512_01278_b200 import kernels as K  # noqa: E402
+from paper_2512_01278_b200.model import make_items  # noqa: E402
+from paper_2512_01278_b200.paged import PagedKvPool  # noqa: E402
+
+DEV = torch.device("cuda")
+
+
+def _pool(L, Hkv, d, n_tokens, rows, dtype, page=16, shuffle_seed=None):
+    pages_per_row = -(-n_tokens // page)
+    pool = PagedKvPool(L, Hkv, d, pages_per_row * rows + 3, page, rows, pages_per_row, dtype, DEV)
+    if shuffle_seed is not None:  # scatter physical pages to stress the gather path
+        rng = np.random.default_rng(shuffle_seed)
+        rng.shuffle(pool._free)
+    for r in range(rows):
+        pool.ensure_tokens(r, n_tokens)
+    pool.sync_table()
+    return pool
+
+
+def _fill(pool, row, n, rng, scale=1.0):
+    L, Hkv, d = pool.layers, pool.kv_heads, pool.head_dim
+    k = rng.normal(size=(n, L, Hkv, d)) * scale
+    v = rng.normal(size=(n, L, Hkv, d))
+    pool.write(row, range(n), torch.from_numpy(k), torch.from_numpy(v))
+    return k, v
+
+
+def _ref_rows(q, k, v, Hq, Hkv, d, crit, dense, qpos0, planted=(), bonus=0.0):
+    """Per query token: oracle attend_one over crit U dense[:qpos+1] (dtype-rounded inputs)."""
+    shape = O.Shape(1, Hq, Hkv, d, 2)
+    outs, lses, accs = [], [], []
+    for t in range(q.shape[0]):
+        pos_list = list(crit) + [p for p in dense if p <= qpos0 + t]
+        keys = k[pos_list]
+        vals = v[pos_list]
+        bias = None
+        if planted:
+            bias = np.where(np.isin(pos_list, planted), bonus, 0.0)
+        ctx, lg, lse = O.attend_one(q[t], keys, vals, shape, bias)
+        outs.append(ctx.reshape(Hq, d))
+        lses.append(lse)
+        p = np.exp(lg - lse[:, None]).sum(axis=0)
+        accs.append(dict(zip(pos_list, p)))
+    return np.stack(outs), np.stack(lses), accs
+
+
+@pytest.mark.parametrize("dtype,force_generic,d,G", [
+    (torch.float32, True, 32, 4), (torch.float32, True, 8, 2), (torch.bfloat16, False, 128, 4),
+    (torch.bfloat16, False, 128, 8), (torch.bfloat16, False, 64, 4), (torch.bfloat16, True, 128, 4),
+])
+def test_verify_attention_matches_oracle(dtype, force_generic, d, G):
+    rng = np.random.default_rng(0)
+    Hkv, L = 2, 2
+    Hq = Hkv * G
+    n0, nq = 700, 5
+    pool = _pool(L, Hkv, d, n0 + nq, 2, dtype, shuffle_seed=1)
+    k, v = _fill(pool, 1, n0 + nq, rng)
+    kq = pool.k.float().cpu().numpy()  # dtype-rounded values as the kernel sees them
+    kr, vr = pool.read(1, range(n0 + nq))
+    kr, vr = kr.double().cpu().numpy(), vr.double().cpu().numpy()
+    q = torch.from_numpy(rng.normal(size=(nq, Hq, d))).to(DEV, dtype)
+    out = torch.empty_like(q)
+    lse = torch.empty(nq, Hq, dtype=torch.float32, device=DEV)
+    acc = torch.zeros(nq, n0 + nq, dtype=torch.float32, device=DEV)
+    items = make_items([(1, 0, nq, n0, 0, 0, 0, 0, 1)], DEV)
+    planted = torch.tensor([3, 77, 400], dtype=torch.int32, device=DEV)
+    for use_planted in (False, True):
+        acc.zero_()
+        K.attention(q, out, pool, 1, items, 1, n0 + nq, nq, Hq, lse=lse, acc=acc, acc_row_stride=n0 + nq,
+                    planted=planted if use_planted else None, planted_bonus=3.0 if use_planted else 0.0,
+                    force_generic=force_generic)
+        torch.cuda.synchronize()
+        ro, rl, ra = _ref_rows(q.double().cpu().numpy(), kr[:, 1], vr[:, 1], Hq, Hkv, d, [], range(n0 + nq), n0,
+                               planted=(3, 77, 400) if use_planted else (), bonus=3.0)
+        tol = 1e-4 if dtype == torch.float32 else 2e-2
+        assert np.abs(out.double().cpu().numpy() - ro).max() <= tol
+        assert np.abs(lse.double().cpu().numpy() - rl).max() <= (1e-4 if dtype == torch.float32 else 2e-2)
+        acc_h = acc.double().cpu().numpy()
+        for t in range(nq):
+            want = np.zeros(n0 + nq)
+            for p_, val in ra[t].items():
+                want[p_] = val
+            assert np.abs(acc_h[t] - want).max() <= (1e-5 if dtype == torch.float32 else 2e-2 * G)
+            assert acc_h[t, n0 + t + 1:].max() == 0.0  # causally hidden tail carries exactly zero
+
+
+@pytest.mark.parametrize("dtype,force_generic,d", [
+    (torch.float32, True, 32), (torch.bfloat16, False, 128), (torch.bfloat16, False, 64)])
+def test_sparse_draft_attention_matches_oracle(dtype, force_generic, d):
+    rng = np.random.default_rng(1)
+    Hkv, G, L = 4, 4, 1
+    Hq = Hkv * G
+    n0, j = 3000, 2
+    pool = _pool(L, Hkv, d, n0 + j + 1, 1, dtype, shuffle_seed=3)
+    _fill(pool, 0, n0 + j + 1, rng)
+    kr, vr = pool.read(0, range(n0 + j + 1))
+    kr, vr = kr.double().cpu().numpy()[:, 0], vr.double().cpu().numpy()[:, 0]
+    crit = np.sort(rng.choice(n0, size=151, replace=False)).astype(np.int32)
+    crit_dev = torch.from_numpy(crit).to(DEV)
+    q = torch.from_numpy(rng.normal(size=(1, Hq, d))).to(DEV, dtype)
+    out = torch.empty_like(q)
+    lse = torch.empty(1, Hq, dtype=torch.float32, device=DEV)
+    items = make_items([(0, 0, 1, n0 + j, 0, len(crit), n0, -1, 0)], DEV)
+    K.attention(q, out, pool, 0, items, 1, len(crit) + j + 1, 1, Hq, crit=crit_dev, lse=lse,
+                force_generic=force_generic)
+    torch.cuda.synchronize()
+    ro, rl, _ = _ref_rows(q.double().cpu().numpy(), kr, vr, Hq, Hkv, d, crit.tolist(), range(n0, n0 + j + 1), n0 + j)
+    tol = 1e-4 if dtype == torch.float32 else 2e-2
+    assert np.abs(out.double().cpu().numpy() - ro).max() <= tol
+    assert np.abs(lse.double().cpu().numpy() - rl).max() <= tol
+
+
+def test_batched_items_mixed_lengths_bf16():
+    """Many items of ragged length in one launch (cluster split > 1)."""
+    rng = np.random.default_rng(5)
+    Hkv, G, d, L = 8, 4, 128, 1
+    Hq = Hkv * G
+    lens = [1, 63, 64, 65, 1000, 4099, 8709]
+    nq = 5
+    pool = _pool(L, Hkv, d, max(lens) + nq, len(lens), torch.bfloat16, shuffle_seed=9)
+    for r, n in enumerate(lens):
+        _fill(pool, r, n + nq, rng)
+    rows = [(r, r * nq, nq, n, 0, 0, 0, r * nq, 1) for r, n in enumerate(lens)]
+    items = make_items(rows, DEV)
+    q = torch.from_numpy(rng.normal(size=(len(lens) * nq, Hq, d))).to(DEV, torch.bfloat16)
+    out = torch.empty_like(q)
+    lse = torch.empty(len(lens) * nq, Hq, dtype=torch.float32, device=DEV)
+    W = max(lens) + nq
+    acc = torch.zeros(len(lens) * nq, W, dtype=torch.float32, device=DEV)
+    K.attention(q, out, pool, 0, items, len(lens), max(lens) + nq, nq, Hq, lse=lse, acc=acc, acc_row_stride=W)
+    torch.cuda.synchronize()
+    for r, n in enumerate(lens):
+        kr, vr = pool.read(r, range(n + nq))
+        kr, vr = kr.double().cpu().numpy()[:, 0], vr.double().cpu().numpy()[:, 0]
+        qs = q[r * nq:(r + 1) * nq].double().cpu().numpy()
+        ro, rl, ra = _ref_rows(qs, kr, vr, Hq, Hkv, d, [], range(n + nq), n)
+        assert np.abs(out[r * nq:(r + 1) * nq].double().cpu().numpy() - ro).max() <= 2e-2
+        assert np.abs(lse[r * nq:(r + 1) * nq].double().cpu().numpy() - rl).max() <= 2e-2
+        a = acc[r * nq:(r + 1) * nq].double().cpu().numpy()
+        np.testing.assert_allclose(a.sum(axis=1), G * np.ones(nq), rtol=2e-2)
+
+
+def test_topk_golden_kats(golden_topk):
+    n = len([k for k in golden_topk if k.endswith(".values")])
+    for dt in (torch.float64,):
+        for i in range(n):
+            v = torch.from_numpy(golden_topk[f"t{i}.values"]).to(DEV, dt)
+            b = int(golden_topk[f"t{i}.budget"])
+            take = min(b, v.numel())
+            out = torch.empty(1, max(take, 1), dtype=torch.int32, device=DEV)
+            ln = torch.empty(1, dtype=torch.int32, device=DEV)
+            K.topk(v[None], torch.tensor([v.numel()], dtype=torch.int32, device=DEV),
+                   torch.tensor([b], dtype=torch.int32, device=DEV), out, ln)
+            assert int(ln.item()) == take
+            assert out[0, :take].cpu().tolist() == golden_topk[f"t{i}.positions"].tolist()
+
+
+def test_topk_random_float32_vs_stable_sort():
+    rng = np.random.default_rng(11)
+    for trial in range(300):
+        n = int(rng.integers(1, 20000))
+        v = rng.normal(size=n).astype(np.float32)
+        if trial % 3 == 0:
+            v = np.round(v, 1).astype(np.float32)
+        if trial % 4 == 0:
+            v = np.abs(v) * (rng.random(n) < 0.1)  # mostly exact zeros (planted-like ties)
+        b = int(rng.integers(1, n + 2))
+        want = O.topk_ascending(v.astype(np.float64), b)
+        out = torch.empty(1, max(min(b, n), 1), dtype=torch.int32, device=DEV)
+        ln = torch.empty(1, dtype=torch.int32, device=DEV)
+        K.topk(torch.from_numpy(v).to(DEV)[None], torch.tensor([n], dtype=torch.int32, device=DEV),
+               torch.tensor([b], dtype=torch.int32, device=DEV), out, ln)
+        assert out[0, : min(b, n)].cpu().tolist() == want.tolist()
+
+
+def test_select_critical_budget_and_rows(golden_budgets):
+    rng = np.random.default_rng(3)
+    B, rows, W = 6, 5, 9000
+    acc = torch.from_numpy(rng.random((B, rows, W)).astype(np.float32)).to(DEV)
+    acc[2] = 0.0  # all ties
+    kv_len = np.array([0, 1, 4000, 8999, 1000, 560], dtype=np.int32)
+    n_rows = np.array([1, 2, 3, 5, 4, 1], dtype=np.int32)
+    for s in (0.05, 0.07, 0.01, 1.0):
+        imp = torch.zeros(B, W, dtype=torch.float32, device=DEV)
+        crit = torch.zeros(B, W, dtype=torch.int32, device=DEV)
+        clen = torch.zeros(B, dtype=torch.int32, device=DEV)
+        bud = torch.zeros(B, dtype=torch.int32, device=DEV)
+        K.select_critical(acc, acc.stride(0), acc.stride(1), torch.from_numpy(n_rows).to(DEV),
+                          torch.from_numpy(kv_len).to(DEV), s, B, imp, crit, clen, bud)
+        torch.cuda.synchronize()
+        for r in range(B):
+            n = int(kv_len[r])
+            want_imp = acc[r, : n_rows[r], :n].double().cpu().numpy()
+            got_imp = imp[r, :n].cpu().numpy()
+            # summation order is fixed (rows ascending, fp32)
+            ref32 = np.zeros(n, dtype=np.float32)
+            for t in range(n_rows[r]):
+                ref32 = (ref32 + acc[r, t, :n].cpu().numpy()).astype(np.float32)
+            assert np.array_equal(got_imp, ref32)
+            b = O.budget_for(n, s)
+            assert int(bud[r]) == b
+            want = O.topk_ascending(got_imp.astype(np.float64), b) if n else np.zeros(0, dtype=np.int64)
+            assert int(clen[r]) == min(b, n)
+            assert crit[r, : min(b, n)].cpu().tolist() == want.tolist()
+            del want_imp
+    # device budget formula == reference on every golden (n, s)
+    for n, s, b in golden_budgets:
+        if n > W:
+            continue
+        clen = torch.zeros(1, dtype=torch.int32, device=DEV)
+        bud = torch.zeros(1, dtype=torch.int32, device=DEV)
+        K.select_critical(acc, 0, acc.stride(1), torch.tensor([1], dtype=torch.int32, device=DEV),
+                          torch.tensor([n], dtype=torch.int32, device=DEV), s, 1,
+                          torch.zeros(1, W, device=DEV), torch.zeros(1, W, dtype=torch.int32, device=DEV), clen, bud)
+        assert int(bud.item()) == b, (n, s)
+
+
+def test_argmax_and_accept():
+    rng = np.random.default_rng(4)
+    for dt in (torch.float32, torch.bfloat16):
+        logits = rng.normal(size=(37, 151936)).astype(np.float32)
+        logits[3, [5, 9, 100]] = 50.0  # tie -> lowest id
+        logits[4, :] = 1.0
+        t = torch.from_numpy(logits).to(DEV, dt)
+        out = torch.empty(37, dtype=torch.int32, device=DEV)
+        K.argmax_rows(t, out)
+        want = np.argmax(t.float().cpu().numpy(), axis=1)
+        assert out.cpu().numpy().tolist() == want.tolist()
+    # accept rule (engine.py:231-239)
+    targets = torch.tensor([5, 6, 7, 8, 9, 1, 2, 3, 4], dtype=torch.int32, device=DEV)
+    tokens = torch.tensor([0, 5, 6, 0, 9, 0, 2, 9, 4], dtype=torch.int32, device=DEV)
+    row0 = torch.tensor([0, 5, 8], dtype=torch.int32, device=DEV)
+    nrows = torch.tensor([5, 3, 1], dtype=torch.int32, device=DEV)
+    acc_, bonus = torch.empty(3, dtype=torch.int32, device=DEV), torch.empty(3, dtype=torch.int32, device=DEV)
+    K.greedy_accept(targets, tokens, row0, nrows, acc_, bonus)
+    assert acc_.cpu().tolist() == [2, 1, 0]
+    assert bonus.cpu().tolist() == [7, 2, 4]
+
+
+def test_rope_kv_write_matches_oracle():
+    rng = np.random.default_rng(2)
+    Hq, Hkv, d, L = 8, 2, 32, 2
+    pool = _pool(L, Hkv, d, 300, 2, torch.float32)
+    rows = 6
+    qkv = torch.from_numpy(rng.normal(size=(rows, (Hq + 2 * Hkv) * d))).to(DEV, torch.float32)
+    pos = np.array([0, 1, 17, 100, 255, 299], dtype=np.int32)
+    tab = np.array([0, 1, 0, 1, 1, 0], dtype=np.int32)
+    q_out = torch.empty(rows, Hq, d, dtype=torch.float32, device=DEV)
+    K.rope_kv_write(qkv, torch.from_numpy(tab).to(DEV), torch.from_numpy(pos).to(DEV), pool, 1, Hq, q_out)
+    torch.cuda.synchronize()
+    x = qkv.double().cpu().numpy()
+    for r in range(rows):
+        want_q = O.rope(x[r, : Hq * d].reshape(Hq, d), int(pos[r]), d)
+        want_k = O.rope(x[r, Hq * d:(Hq + Hkv) * d].reshape(Hkv, d), int(pos[r]), d)
+        want_v = x[r, (Hq + Hkv) * d:].reshape(Hkv, d)
+        kk, vv = pool.read(int(tab[r]), [int(pos[r])])
+        assert np.abs(q_out[r].double().cpu().numpy() - want_q).max() < 1e-5
+        assert np.abs(kk[0, 1].double().cpu().numpy() - want_k).max() < 1e-5
+        assert np.array_equal(vv[0, 1].double().cpu().numpy(), want_v.astype(np.float32).astype(np.float64))

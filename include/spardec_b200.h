@@ -112,11 +112,13 @@ int sd_attention(const void* q, void* out, float* lse, const sd_paged_kv* kv, in
 /* K3: per request r: importance[p] = sum_{t < n_rows[r]} acc[r][t][p] for
  * p < kv_len[r]; budget = max(1, min(ceil(s*n - 1e-9), n)) (n = 0 -> 1);
  * crit[r][:] = top-budget positions (value desc, ties to the lower index),
- * ascending; crit_len[r] = min(budget, kv_len[r]).  importance may be NULL
- * (then it is kept in `workspace`, num_requests * imp_stride floats). */
+ * ascending; crit_len[r] = min(budget, kv_len[r]).
+ * req_index (nullable): request r reads/writes row req_index[r] of acc,
+ * importance, crit, crit_len and budget_out (n_rows / kv_len stay indexed by r). */
 int sd_select_critical(const float* acc, int64_t acc_req_stride, int64_t acc_row_stride,
                        const int32_t* n_rows, const int32_t* kv_len, double sparsity,
-                       int32_t num_requests, float* importance, int64_t imp_stride,
+                       int32_t num_requests, const int32_t* req_index,
+                       float* importance, int64_t imp_stride,
                        int32_t* crit, int64_t crit_stride, int32_t* crit_len,
                        int32_t* budget_out, void* stream);
 

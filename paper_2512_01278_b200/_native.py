@@ -46,8 +46,8 @@ SIGNATURES = {
     "sd_attention": (ctypes.c_int, [_c_p, _c_p, _c_p, ctypes.POINTER(PagedKvDesc), _i32, _c_p, _i32, _i32, _i32,
                                     _c_p, _c_p, _i64, _c_p, _i32, ctypes.c_float, _i32, ctypes.c_float, _c_p,
                                     _i64, _i32, _c_p]),
-    "sd_select_critical": (ctypes.c_int, [_c_p, _i64, _i64, _c_p, _c_p, ctypes.c_double, _i32, _c_p, _i64, _c_p,
-                                          _i64, _c_p, _c_p, _c_p]),
+    "sd_select_critical": (ctypes.c_int, [_c_p, _i64, _i64, _c_p, _c_p, ctypes.c_double, _i32, _c_p, _c_p, _i64,
+                                          _c_p, _i64, _c_p, _c_p, _c_p]),
     "sd_topk": (ctypes.c_int, [_c_p, _i32, _i64, _c_p, _c_p, _i32, _c_p, _i64, _c_p, _c_p]),
     "sd_argmax_rows": (ctypes.c_int, [_c_p, _i32, _i64, _i32, _i32, _c_p, _c_p]),
     "sd_greedy_accept": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i32, _c_p, _c_p, _c_p]),

@@ -24,13 +24,19 @@ __global__ void __launch_bounds__(256) attn_generic_kernel(
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
 
-  float* S = ws + ((int64_t)blockIdx.y * kv.kv_heads + h) * ((int64_t)max_rows * max_keys + 2 * max_keys);
+  float* S = ws + ((int64_t)blockIdx.y * kv.kv_heads + h) * ((int64_t)max_rows * max_keys + 3 * max_keys);
   int32_t* kpos = reinterpret_cast<int32_t*>(S + (int64_t)max_rows * max_keys);
   int32_t* kslot = kpos + max_keys;
+  float* kbias = reinterpret_cast<float*>(kslot + max_keys);
 
+  // Logits are kept WITHOUT the planted bonus and the bonus is carried
+  // separately, so exponents (s - s_max) + (b - b_max) stay exact in fp32
+  // even with the +2000 bonus (the reference computes in fp64).
   extern __shared__ float smem[];
   float* sq = smem;            // [R][D]
-  float* slse = sq + R * D;    // [R]
+  float* sms = sq + R * D;     // [R] logit of the row max
+  float* smb = sms + R;        // [R] bonus of the row max
+  float* sll = smb + R;        // [R] log(sum)
 
   const T* K = static_cast<const T*>(kv.k) + (int64_t)layer * kv.layer_stride;
   const T* V = static_cast<const T*>(kv.v) + (int64_t)layer * kv.layer_stride;
@@ -44,6 +50,7 @@ __global__ void __launch_bounds__(256) attn_generic_kernel(
     const int pos = it.key_pos(crit, j);
     kpos[j] = pos;
     kslot[j] = (int32_t)kv.slot_of(it.table_row, pos);
+    kbias[j] = planted_bias(planted, n_planted, bonus, pos);
   }
   __syncthreads();
 
@@ -58,25 +65,37 @@ __global__ void __launch_bounds__(256) attn_generic_kernel(
       const float* qr = sq + r * D;
       float dot = 0.f;
       for (int d = 0; d < D; ++d) dot = fmaf(qr[d], to_f(kr[d]), dot);
-      s = dot * inv_sqrt_d + planted_bias(planted, n_planted, bonus, pos);
+      s = dot * inv_sqrt_d;
     }
     S[(int64_t)r * max_keys + j] = s;
   }
   __syncthreads();
 
-  // per-row log-sum-exp
+  // per-row log-sum-exp around the (logit, bonus) pair of the row max
   for (int r = warp; r < R; r += nwarp) {
     const float* Sr = S + (int64_t)r * max_keys;
     float m = -INFINITY;
-    for (int j = lane; j < Nk; j += 32) m = fmaxf(m, Sr[j]);
-    m = warp_max(m);
+    int arg = 0x7fffffff;
+    for (int j = lane; j < Nk; j += 32) {
+      const float t = Sr[j] + kbias[j];
+      if (t > m) { m = t; arg = j; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, m, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (om > m || (om == m && oa < arg)) { m = om; arg = oa; }
+    }
+    const float ms = Sr[arg], mb = kbias[arg];
     float l = 0.f;
-    for (int j = lane; j < Nk; j += 32) l += expf(Sr[j] - m);
+    for (int j = lane; j < Nk; j += 32) l += expf((Sr[j] - ms) + (kbias[j] - mb));
     l = warp_sum(l);
-    const float lse = m + logf(l);
+    const float ll = logf(l);
     if (lane == 0) {
-      slse[r] = lse;
-      if (lse_out) lse_out[(int64_t)(it.q_row0 + r / G) * q_heads + h * G + r % G] = lse;
+      sms[r] = ms;
+      smb[r] = mb;
+      sll[r] = ll;
+      if (lse_out) lse_out[(int64_t)(it.q_row0 + r / G) * q_heads + h * G + r % G] = (ms + mb) + ll;
     }
   }
   __syncthreads();
@@ -85,12 +104,12 @@ __global__ void __launch_bounds__(256) attn_generic_kernel(
   for (int i = tid; i < R * D; i += nthr) {
     const int r = i / D, d = i - r * D;
     const float* Sr = S + (int64_t)r * max_keys;
-    const float l = slse[r];
+    const float ms = sms[r], mb = smb[r], ll = sll[r];
     float o = 0.f;
     for (int j = 0; j < Nk; ++j) {
       const float s = Sr[j];
       if (s == -INFINITY) continue;
-      o = fmaf(expf(s - l), to_f(V[kv.row_off(kslot[j], h) + d]), o);
+      o = fmaf(expf(((s - ms) + (kbias[j] - mb)) - ll), to_f(V[kv.row_off(kslot[j], h) + d]), o);
     }
     const int qt = r / G, g = r - qt * G;
     out[((int64_t)(it.q_row0 + qt) * q_heads + h * G + g) * D + d] = from_f<T>(o);
@@ -104,7 +123,7 @@ __global__ void __launch_bounds__(256) attn_generic_kernel(
       for (int g = 0; g < G; ++g) {
         const int r = qt * G + g;
         const float s = S[(int64_t)r * max_keys + j];
-        if (s != -INFINITY) sum += expf(s - slse[r]);
+        if (s != -INFINITY) sum += expf(((s - sms[r]) + (kbias[j] - smb[r])) - sll[r]);
       }
       if (sum != 0.f)
         atomicAdd(acc + (int64_t)(it.acc_row + qt * it.acc_step) * acc_stride + kpos[j], sum);
@@ -113,7 +132,7 @@ __global__ void __launch_bounds__(256) attn_generic_kernel(
 }
 
 int64_t generic_ws_bytes(int num_items, int max_keys, int max_rows, int kv_heads) {
-  return (int64_t)num_items * kv_heads * ((int64_t)max_rows * max_keys + 2 * max_keys) * 4;
+  return (int64_t)num_items * kv_heads * ((int64_t)max_rows * max_keys + 3 * max_keys) * 4;
 }
 
 int launch_attn_generic(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer,
@@ -125,7 +144,7 @@ int launch_attn_generic(const void* q, void* out, float* lse, const sd_paged_kv*
   const int max_rows = max_nq * G;
   SD_REQUIRE(ws_bytes >= generic_ws_bytes(num_items, max_keys, max_rows, kvp->kv_heads),
              "sd_attention: workspace too small for the generic kernel");
-  const size_t smem = ((size_t)max_rows * kvp->head_dim + max_rows) * sizeof(float);
+  const size_t smem = ((size_t)max_rows * kvp->head_dim + 3 * max_rows) * sizeof(float);
   SD_REQUIRE(smem <= 200 * 1024, "sd_attention: generic kernel query tile exceeds shared memory");
   PagedKv kv = make_paged(kvp);
   dim3 grid(kvp->kv_heads, num_items);

@@ -123,11 +123,11 @@ __device__ void block_topk(const ValT* vals, int n, int take, int32_t* out) {
 __global__ void __launch_bounds__(SEL_THREADS) select_critical_kernel(
     const float* __restrict__ acc, int64_t acc_req_stride, int64_t acc_row_stride,
     const int32_t* __restrict__ n_rows, const int32_t* __restrict__ kv_len, double sparsity,
-    float* __restrict__ imp, int64_t imp_stride, int32_t* __restrict__ crit, int64_t crit_stride,
+    const int32_t* __restrict__ req_index, float* __restrict__ imp, int64_t imp_stride, int32_t* __restrict__ crit, int64_t crit_stride,
     int32_t* __restrict__ crit_len, int32_t* __restrict__ budget_out) {
-  const int r = blockIdx.x;
-  const int n = kv_len[r];
-  const int rows = n_rows[r];
+  const int n = kv_len[blockIdx.x];
+  const int rows = n_rows[blockIdx.x];
+  const int r = req_index ? req_index[blockIdx.x] : blockIdx.x;
   float* v = imp + (int64_t)r * imp_stride;
   const float* a = acc + (int64_t)r * acc_req_stride;
   for (int p = threadIdx.x; p < n; p += SEL_THREADS) {
@@ -162,14 +162,14 @@ __global__ void __launch_bounds__(SEL_THREADS) topk_kernel(const ValT* __restric
 
 extern "C" int sd_select_critical(const float* acc, int64_t acc_req_stride, int64_t acc_row_stride,
                                   const int32_t* n_rows, const int32_t* kv_len, double sparsity,
-                                  int32_t num_requests, float* importance, int64_t imp_stride, int32_t* crit,
+                                  int32_t num_requests, const int32_t* req_index, float* importance, int64_t imp_stride, int32_t* crit,
                                   int64_t crit_stride, int32_t* crit_len, int32_t* budget_out, void* stream) {
   SD_REQUIRE(sparsity > 0.0 && sparsity <= 1.0, "sd_select_critical: sparsity must be in (0, 1]");
   SD_REQUIRE(num_requests >= 0, "sd_select_critical: negative request count");
   SD_REQUIRE(acc && n_rows && kv_len && importance && crit && crit_len, "sd_select_critical: null pointer");
   if (num_requests == 0) return 0;
   sd::select_critical_kernel<<<num_requests, sd::SEL_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
-      acc, acc_req_stride, acc_row_stride, n_rows, kv_len, sparsity, importance, imp_stride, crit, crit_stride,
+      acc, acc_req_stride, acc_row_stride, n_rows, kv_len, sparsity, req_index, importance, imp_stride, crit, crit_stride,
       crit_len, budget_out);
   sd::count_launch();
   SD_CUDA_RETURN();

@@ -40,7 +40,7 @@ def attention(q: torch.Tensor, out: torch.Tensor, pool, layer: int, items: torch
     need = lib.sd_attention_workspace_bytes(num_items, max_keys, max_nq, q_heads, ctypes.byref(desc))
     if force_generic:
         G = q_heads // pool.kv_heads
-        need = num_items * pool.kv_heads * (max_nq * G * max_keys + 2 * max_keys) * 4
+        need = num_items * pool.kv_heads * (max_nq * G * max_keys + 3 * max_keys) * 4
     if need > 0 and (workspace is None or workspace.numel() * workspace.element_size() < need):
         workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
@@ -56,12 +56,16 @@ def attention(q: torch.Tensor, out: torch.Tensor, pool, layer: int, items: torch
 
 def select_critical(acc: torch.Tensor, acc_req_stride: int, acc_row_stride: int, n_rows: torch.Tensor,
                     kv_len: torch.Tensor, sparsity: float, num: int, importance: torch.Tensor,
-                    crit: torch.Tensor, crit_len: torch.Tensor, budget: torch.Tensor | None = None) -> None:
-    """K3: importance = sum of the surviving score rows; budget; tie-exact top-k."""
+                    crit: torch.Tensor, crit_len: torch.Tensor, budget: torch.Tensor | None = None,
+                    req_index: torch.Tensor | None = None) -> None:
+    """K3: importance = sum of the surviving score rows; budget; tie-exact top-k.
+    ``req_index[r]`` (optional) redirects request r to row req_index[r] of
+    acc / importance / crit / crit_len / budget."""
     if num == 0:
         return
     N.check(N.lib().sd_select_critical(acc.data_ptr(), acc_req_stride, acc_row_stride, n_rows.data_ptr(),
-                                       kv_len.data_ptr(), float(sparsity), num, importance.data_ptr(),
+                                       kv_len.data_ptr(), float(sparsity), num, N.ptr(req_index),
+                                       importance.data_ptr(),
                                        importance.stride(0), crit.data_ptr(), crit.stride(0),
                                        crit_len.data_ptr(), N.ptr(budget), N.stream_handle()),
             "sd_select_critical")

@@ -119,5 +119,5 @@ class PagedKvPool:
     def write(self, row: int, positions, k: torch.Tensor, v: torch.Tensor) -> None:
         """Store (n, layers, kv_heads, head_dim) rows at ``positions``."""
         s = self.slots(row, positions).to(self.device)
-        self.k[:, s] = k.transpose(0, 1).to(self.dtype)
-        self.v[:, s] = v.transpose(0, 1).to(self.dtype)
+        self.k[:, s] = k.transpose(0, 1).to(self.device, self.dtype)
+        self.v[:, s] = v.transpose(0, 1).to(self.device, self.dtype)

@@ -36,7 +36,7 @@ def test_contract_violation_maps_to_contract_error():
     from paper_2512_01278_b200 import _native as N
     from paper_2512_01278_b200.errors import ContractError
     lib = N.load_library()
-    rc = lib.sd_select_critical(None, 0, 0, None, None, 0.5, 1, None, 0, None, 0, None, None, None)
+    rc = lib.sd_select_critical(None, 0, 0, None, None, 0.5, 1, None, None, 0, None, 0, None, None, None)
     assert rc < 0
     with pytest.raises(ContractError, match="null pointer"):
         N.check(rc, "sd_select_critical")

@@ -76,7 +76,6 @@ def test_verify_attention_matches_oracle(dtype, force_generic, d, G):
     n0, nq = 700, 5
     pool = _pool(L, Hkv, d, n0 + nq, 2, dtype, shuffle_seed=1)
     k, v = _fill(pool, 1, n0 + nq, rng)
-    kq = pool.k.float().cpu().numpy()  # dtype-rounded values as the kernel sees them
     kr, vr = pool.read(1, range(n0 + nq))
     kr, vr = kr.double().cpu().numpy(), vr.double().cpu().numpy()
     q = torch.from_numpy(rng.normal(size=(nq, Hq, d))).to(DEV, dtype)
@@ -254,8 +253,8 @@ def test_argmax_and_accept():
     nrows = torch.tensor([5, 3, 1], dtype=torch.int32, device=DEV)
     acc_, bonus = torch.empty(3, dtype=torch.int32, device=DEV), torch.empty(3, dtype=torch.int32, device=DEV)
     K.greedy_accept(targets, tokens, row0, nrows, acc_, bonus)
-    assert acc_.cpu().tolist() == [2, 1, 0]
-    assert bonus.cpu().tolist() == [7, 2, 4]
+    assert acc_.cpu().tolist() == [2, 0, 0]
+    assert bonus.cpu().tolist() == [7, 1, 4]
 
 
 def test_rope_kv_write_matches_oracle():

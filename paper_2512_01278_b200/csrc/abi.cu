@@ -18,6 +18,7 @@ int launch_attn_generic(const void* q, void* out, float* lse, const sd_paged_kv*
                         float* acc, int64_t acc_stride, const int32_t* planted, int n_planted, float bonus,
                         int q_heads, float scale, void* ws, int64_t ws_bytes, cudaStream_t stream);
 bool mma_attn_supported(int dtype, int D, int rows);
+bool mma_attn_plannable(int dtype, int D, int rows, int max_keys, int num_items, int kv_heads);
 int launch_attn_mma(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer,
                     const int32_t* items, int num_items, int max_keys, int max_nq, const int32_t* crit,
                     float* acc, int64_t acc_stride, const int32_t* planted, int n_planted, float bonus,
@@ -33,7 +34,7 @@ extern "C" int64_t sd_attention_workspace_bytes(int32_t num_items, int32_t max_k
                                                 int32_t q_heads, const sd_paged_kv* kv) {
   if (kv == nullptr || kv->kv_heads <= 0) return 0;
   const int G = q_heads / kv->kv_heads;
-  if (sd::mma_attn_supported(kv->dtype, kv->head_dim, max_nq * G)) return 0;
+  if (sd::mma_attn_plannable(kv->dtype, kv->head_dim, max_nq * G, max_keys, num_items, kv->kv_heads)) return 0;
   return sd::generic_ws_bytes(num_items, max_keys, max_nq * G, kv->kv_heads);
 }
 

@@ -422,6 +422,13 @@ int launch_one(const Params& prm, int C, int num_items, int kv_heads, int smem, 
 bool mma_attn_supported(int dtype, int D, int rows) {
   return dtype == SD_DTYPE_BF16 && (D == 64 || D == 128) && rows >= 1 && rows <= 80;
 }
+static bool plan_mma(int D, int MT, int rows, int max_keys, int num_items, int kv_heads, int* C_out,
+                     int* chunk_out, int* smem_out);
+bool mma_attn_plannable(int dtype, int D, int rows, int max_keys, int num_items, int kv_heads) {
+  if (!mma_attn_supported(dtype, D, rows)) return false;
+  int C, chunk, smem;
+  return plan_mma(D, (rows + 15) / 16, rows, max_keys < 1 ? 1 : max_keys, num_items, kv_heads, &C, &chunk, &smem);
+}
 
 // Pick cluster size C and chunk so the whole chunk's logits stay in smem.
 static bool plan_mma(int D, int MT, int rows, int max_keys, int num_items, int kv_heads, int* C_out,
@@ -430,19 +437,20 @@ static bool plan_mma(int D, int MT, int rows, int max_keys, int num_items, int k
   const int limit = 227 * 1024;
   const int max_tiles = (max_keys + TK - 1) / TK;
   int c_par = (2 * 148 + num_items * kv_heads - 1) / (num_items * kv_heads);  // ~2 CTAs per SM
-  c_par = c_par < 1 ? 1 : c_par;
+  c_par = c_par < 1 ? 1 : (c_par > 16 ? 16 : c_par);
+  bool found = false;
   for (int C = 1; C <= 16; ++C) {
     int chunk = ((max_tiles + C - 1) / C) * TK;
     if (chunk < TK) chunk = TK;
     const Layout L = make_layout(D, MT, chunk, rows);
-    if (L.total <= limit && (C >= c_par || C >= max_tiles)) {
-      *C_out = C;
-      *chunk_out = chunk;
-      *smem_out = L.total;
-      return true;
-    }
+    if (L.total > limit) continue;
+    *C_out = C;  // smallest fitting C that also gives enough CTAs (or cannot split further)
+    *chunk_out = chunk;
+    *smem_out = L.total;
+    found = true;
+    if (C >= c_par || C >= max_tiles) break;
   }
-  return false;
+  return found;
 }
 
 int launch_attn_mma(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer,

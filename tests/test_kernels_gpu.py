@@ -101,7 +101,8 @@ def test_verify_attention_matches_oracle(dtype, force_generic, d, G):
             for p_, val in ra[t].items():
                 want[p_] = val
             assert np.abs(acc_h[t] - want).max() <= (1e-5 if dtype == torch.float32 else 2e-2 * G)
-            assert acc_h[t, n0 + t + 1:].max() == 0.0  # causally hidden tail carries exactly zero
+            if n0 + t + 1 < acc_h.shape[1]:
+                assert acc_h[t, n0 + t + 1:].max() == 0.0  # causally hidden tail carries exactly zero
 
 
 @pytest.mark.parametrize("dtype,force_generic,d", [
@@ -157,7 +158,13 @@ def test_batched_items_mixed_lengths_bf16():
         assert np.abs(out[r * nq:(r + 1) * nq].double().cpu().numpy() - ro).max() <= 2e-2
         assert np.abs(lse[r * nq:(r + 1) * nq].double().cpu().numpy() - rl).max() <= 2e-2
         a = acc[r * nq:(r + 1) * nq].double().cpu().numpy()
-        np.testing.assert_allclose(a.sum(axis=1), G * np.ones(nq), rtol=2e-2)
+        # each query's probabilities sum to 1 per q head: Hq in total
+        np.testing.assert_allclose(a.sum(axis=1), Hq * np.ones(nq), rtol=2e-2)
+        for t in range(nq):
+            want = np.zeros(W)
+            for p_, val in ra[t].items():
+                want[p_] = val
+            assert np.abs(a[t] - want).max() <= 2e-2
 
 
 def test_topk_golden_kats(golden_topk):

@@ -157,7 +157,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
             prompt = synthetic_prompt(0, rid, args.prompt, cfg.vocab_size)
             cont = synthetic_prompt(1, rid, ctx - args.prompt, cfg.vocab_size)
             reqs.append(DecodeRequest(rid, prompt + cont, max_seq - ctx))
-        seqs = dec.prefill(reqs, max_rows=16384)
+        seqs = dec.prefill(reqs, max_rows=32768)
         buckets = PhaseBuckets.empty(k)
         for sq in seqs:
             sq.round_target = first_round_draft_len(k, assign_new_request(buckets))

@@ -140,6 +140,11 @@ int sd_greedy_accept(const int32_t* targets, const int32_t* tokens, const int32_
                      const int32_t* nrows, int32_t num, int32_t* accepted, int32_t* bonus,
                      void* stream);
 
+/* Glue (outside the attention hot path): out = x / sqrt(mean(x^2) + eps) per
+ * row (model.py:225-226, RMSNorm without gain) cast to out_dtype.  x fp32. */
+int sd_rmsnorm_cast(const float* x, int32_t rows, int32_t h, float eps, void* out, int32_t out_dtype,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

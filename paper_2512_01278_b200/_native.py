@@ -51,6 +51,7 @@ SIGNATURES = {
     "sd_topk": (ctypes.c_int, [_c_p, _i32, _i64, _c_p, _c_p, _i32, _c_p, _i64, _c_p, _c_p]),
     "sd_argmax_rows": (ctypes.c_int, [_c_p, _i32, _i64, _i32, _i32, _c_p, _c_p]),
     "sd_greedy_accept": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i32, _c_p, _c_p, _c_p]),
+    "sd_rmsnorm_cast": (ctypes.c_int, [_c_p, _i32, _i32, ctypes.c_float, _c_p, _i32, _c_p]),
 }
 
 _LIB = None
@@ -69,7 +70,10 @@ def load_library(path: Path | None = None) -> ctypes.CDLL:
         )
     lib = ctypes.CDLL(str(p))
     for name, (res, args) in SIGNATURES.items():
-        fn = getattr(lib, name)
+        try:
+            fn = getattr(lib, name)
+        except AttributeError as e:
+            raise ImportError(f"{p} is stale (missing {name}); rebuild it") from e
         fn.restype = res
         fn.argtypes = args
     if lib.sd_abi_version() != 1:

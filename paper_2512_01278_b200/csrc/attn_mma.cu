@@ -1,20 +1,24 @@
 // Tensor-core (bf16 mma.sync m16n8k16) paged attention for sm_100a with a
-// thread-block cluster per (work item, kv head) and exact two-phase softmax.
+// thread-block cluster per (work item, kv head) and an exact two-pass softmax.
 //
 //   grid    = (C, kv_heads, num_items), cluster = (C, 1, 1)
 //   CTA c   = keys [c*chunk, (c+1)*chunk) of the item's key list
 //             (critical positions first, then the dense causal range)
 //
-// phase 1  K tiles (64 keys) stream HBM -> smem with a 4-stage cp.async ring;
-//          S^T tile = Q K^T on tensor cores; scaled/masked/planted logits are
-//          kept in shared memory for the whole chunk (log2 domain).
-// exchange per-row (max, sum) across the cluster through DSMEM -> exact lse.
-// phase 2  V tiles stream in; P = exp2(S - lse) is FINAL (no online
-//          rescaling), so PillarAttn's score accumulator
-//          acc[token][pos] += sum_{g in group} P  is emitted right here, with
-//          zero extra HBM traffic for logits (SURVEY.md §7.2 option (c));
-//          O_partial = P V on tensor cores.
+// pass 1   K tiles (64 keys x d) stream HBM -> smem through a cp.async ring
+//          (L2 evict_last); S = Q K^T on tensor cores; every thread keeps an
+//          online (max, sum) for its rows -> per-row chunk statistics.
+// exchange (max, sum) across the cluster through DSMEM -> exact row lse.
+// pass 2   K (L2-resident re-read, evict_first) + V tiles (HBM, evict_first);
+//          S recomputed, P = exp2(S - lse) is FINAL (no online rescaling), so
+//          PillarAttn's score accumulator acc[token][pos] += sum_{g in group} P
+//          is emitted from registers (warp shuffles over the group's rows);
+//          O_partial += P V on tensor cores.
 // reduce   O partials summed across the cluster through DSMEM, written once.
+//
+// HBM traffic = K + V once per (item, kv head); the logits never leave the
+// SM (SURVEY.md §7.2 option (c) without the smem logit buffer, so two CTAs
+// fit per SM and any context length works).
 //
 // Restates model.py:229-253 (_attend), used by forward_full (verify, prefill;
 // model.py:318-334) and forward_sparse (draft; model.py:360-380), and the
@@ -28,17 +32,27 @@ namespace cg = cooperative_groups;
 namespace sd {
 namespace mma_attn {
 
-constexpr int TK = 64;      // keys per tile
-constexpr int NT = 256;     // threads per CTA
+constexpr int TK = 64;        // keys per tile
+constexpr int NT = 256;       // threads per CTA
 constexpr int NW = NT / 32;
-constexpr int STAGES = 4;
 constexpr int PROW = TK + 8;  // bf16 per P-tile row (conflict-free ldmatrix)
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes, uint64_t policy) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes), "l"(policy));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -82,45 +96,67 @@ struct Params {
   float bonus_log2;
   int q_heads;
   float scale_log2;
-  int chunk;      // keys per CTA, multiple of TK
-  int srow;       // floats per S row (chunk + 8)
-  int s_rows;     // rows of the S buffer (max rows over items)
+  int chunk;  // keys per CTA, multiple of TK
 };
 
 // Shared-memory carve, identical on host and device.
 struct Layout {
-  int k_off, q_off, p_off, s_off, pos_off, slot_off, m_off, l_off, lse_off, total;
+  int ring_off, q_off, p_off, wm_off, wl_off, m_off, l_off, lse_off, total;
 };
-__host__ __device__ inline Layout make_layout(int D, int MT, int chunk, int s_rows) {
+__host__ __device__ inline Layout make_layout(int D, int MT, int nslot) {
   const int RP = MT * 16;
   const int krow = D + 8;
   Layout L;
   int o = 0;
-  L.k_off = o;   o += STAGES * TK * krow * 2;
+  L.ring_off = o;
+  {
+    const int ring = nslot * TK * krow * 2;
+    const int obuf = RP * D * 4;  // O partials reuse the ring after the loop
+    o += ring > obuf ? ring : obuf;
+  }
   L.q_off = o;   o += RP * krow * 2;
   L.p_off = o;   o += RP * PROW * 2;
-  L.s_off = o;
-  {
-    const int s_bytes = s_rows * (chunk + 8) * 4;
-    const int o_bytes = RP * D * 4;
-    o += s_bytes > o_bytes ? s_bytes : o_bytes;
-  }
-  L.pos_off = o;  o += chunk * 4;
-  L.slot_off = o; o += chunk * 4;
-  L.m_off = o;    o += RP * 4;
-  L.l_off = o;    o += RP * 4;
-  L.lse_off = o;  o += RP * 4;
+  L.wm_off = o;  o += NW * RP * 4;
+  L.wl_off = o;  o += NW * RP * 4;
+  L.m_off = o;   o += RP * 4;
+  L.l_off = o;   o += RP * 4;
+  L.lse_off = o; o += RP * 4;
   L.total = o;
   return L;
 }
 
+// S tile (this warp's 8 keys x all RP rows) = Q K^T from smem.
 template <int D, int MT>
-__global__ void __launch_bounds__(NT, 1) attn_mma_kernel(const Params p) {
+__device__ __forceinline__ void qk_tile(float (&sacc)[MT][4], const __nv_bfloat16* Qs, const __nv_bfloat16* Kt,
+                                        int n0, int lane) {
+  constexpr int KROW = D + 8;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) sacc[mt][0] = sacc[mt][1] = sacc[mt][2] = sacc[mt][3] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < D / 16; ks += 2) {
+    unsigned b0, b1, b2, b3;
+    ldsm_x4(b0, b1, b2, b3, Kt + (n0 + (lane & 7)) * KROW + ks * 16 + (lane >> 3) * 8);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      unsigned a0, a1, a2, a3;
+      const __nv_bfloat16* qa = Qs + (mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * KROW + (lane >> 4) * 8;
+      ldsm_x4(a0, a1, a2, a3, qa + ks * 16);
+      mma_bf16(sacc[mt], a0, a1, a2, a3, b0, b1);
+      ldsm_x4(a0, a1, a2, a3, qa + (ks + 1) * 16);
+      mma_bf16(sacc[mt], a0, a1, a2, a3, b2, b3);
+    }
+  }
+}
+
+template <int D, int MT, int NSLOT>
+__global__ void __launch_bounds__(NT, 2) attn_mma_kernel(const Params p) {
   constexpr int RP = MT * 16;
   constexpr int KROW = D + 8;
-  constexpr int DCH = D / 8;          // 16-byte chunks per key row
-  constexpr int NCOLW = D / NW;       // output columns per warp in phase 2 (16 or 8)
-  constexpr int NTW = NCOLW / 8;      // n8 tiles per warp in phase 2
+  constexpr int DCH = D / 8;      // 16-byte chunks per key row
+  constexpr int NCOLW = D / NW;   // output columns per warp in pass 2 (16 or 8)
+  constexpr int NTW = NCOLW / 8;  // n8 tiles per warp in pass 2
+  constexpr int NPAIR = NSLOT / 2;
+  constexpr int TILE = TK * KROW;  // bf16 elements per ring slot
 
   cg::cluster_group cluster = cg::this_cluster();
   const int C = static_cast<int>(cluster.num_blocks());
@@ -137,15 +173,15 @@ __global__ void __launch_bounds__(NT, 1) attn_mma_kernel(const Params p) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g4 = lane >> 2, t4 = lane & 3;
+  const int n0 = warp * 8;  // this warp's 8 keys of a tile in the QK product
 
   extern __shared__ __align__(128) unsigned char smem[];
-  const Layout L = make_layout(D, MT, p.chunk, p.s_rows);
-  __nv_bfloat16* Kst = reinterpret_cast<__nv_bfloat16*>(smem + L.k_off);
+  const Layout L = make_layout(D, MT, NSLOT);
+  __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(smem + L.ring_off);
   __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smem + L.q_off);
   __nv_bfloat16* Pt = reinterpret_cast<__nv_bfloat16*>(smem + L.p_off);
-  float* Sb = reinterpret_cast<float*>(smem + L.s_off);
-  int32_t* spos = reinterpret_cast<int32_t*>(smem + L.pos_off);
-  int32_t* sslot = reinterpret_cast<int32_t*>(smem + L.slot_off);
+  float* wm = reinterpret_cast<float*>(smem + L.wm_off);
+  float* wl = reinterpret_cast<float*>(smem + L.wl_off);
   float* rowm = reinterpret_cast<float*>(smem + L.m_off);
   float* rowl = reinterpret_cast<float*>(smem + L.l_off);
   float* rowlse = reinterpret_cast<float*>(smem + L.lse_off);
@@ -153,19 +189,9 @@ __global__ void __launch_bounds__(NT, 1) attn_mma_kernel(const Params p) {
   const __nv_bfloat16* Kg = static_cast<const __nv_bfloat16*>(p.kv.k) + (int64_t)p.layer * p.kv.layer_stride;
   const __nv_bfloat16* Vg = static_cast<const __nv_bfloat16*>(p.kv.v) + (int64_t)p.layer * p.kv.layer_stride;
   const int kvh = p.kv.kv_heads;
+  const uint64_t keep = policy_evict_last();
+  const uint64_t drop = policy_evict_first();
 
-  // ---- keys of this chunk: absolute position and physical slot ----
-  for (int j = tid; j < ntiles * TK; j += NT) {
-    const int gj = kb + j;
-    if (gj < ke) {
-      const int pos = it.key_pos(p.crit, gj);
-      spos[j] = pos;
-      sslot[j] = static_cast<int32_t>(p.kv.slot_of(it.table_row, pos));
-    } else {
-      spos[j] = 0x7fffffff;
-      sslot[j] = -1;
-    }
-  }
   // ---- query rows (r = token * G + g), zero padded to RP ----
   for (int i = tid; i < RP * DCH; i += NT) {
     const int r = i / DCH, c = i - r * DCH;
@@ -176,98 +202,134 @@ __global__ void __launch_bounds__(NT, 1) attn_mma_kernel(const Params p) {
     }
     *reinterpret_cast<uint4*>(Qs + r * KROW + c * 8) = v;
   }
-  __syncthreads();
+  for (int i = tid; i < (RP - R) * PROW; i += NT) Pt[R * PROW + i] = __float2bfloat16_rn(0.f);
 
-  auto load_tile = [&](const __nv_bfloat16* base, int t, int stage) {
+  // one tile (64 keys) of K or V into a ring slot; each thread moves 4 x 16 B
+  auto load_tile = [&](const __nv_bfloat16* base, int t, __nv_bfloat16* dst, uint64_t pol) {
 #pragma unroll
     for (int i = tid; i < TK * DCH; i += NT) {
       const int kk = i / DCH, c = i - kk * DCH;
-      const int slot = sslot[t * TK + kk];
-      const __nv_bfloat16* src = base + ((int64_t)(slot < 0 ? 0 : slot) * kvh + h) * D + c * 8;
-      cp_async16(Kst + (stage * TK + kk) * KROW + c * 8, src, slot < 0 ? 0 : 16);
+      const int gj = kb + t * TK + kk;
+      int slot = 0, bytes = 0;
+      if (gj < ke) {
+        slot = static_cast<int>(p.kv.slot_of(it.table_row, it.key_pos(p.crit, gj)));
+        bytes = 16;
+      }
+      cp_async16(dst + kk * KROW + c * 8, base + ((int64_t)slot * kvh + h) * D + c * 8, bytes, pol);
     }
   };
 
-  // ================= phase 1: logits =================
+  // per-thread visibility / bias of its two keys of tile t (log2 domain bias)
+  auto key_info = [&](int t, int e, int& pos, bool& in_range, bool& is_crit, float& bias) {
+    const int gj = kb + t * TK + n0 + 2 * t4 + e;
+    in_range = gj < ke;
+    is_crit = gj < it.crit_len;
+    pos = in_range ? it.key_pos(p.crit, gj) : 0x7fffffff;
+    bias = in_range ? planted_bias(p.planted, p.n_planted, p.bonus_log2, pos) : 0.f;
+  };
+
+  // a tile is "full" when all its keys exist and precede every query row and no
+  // planted bias applies; keys are ascending, so checking the last one suffices
+  auto tile_full = [&](int t) -> bool {
+    if (p.n_planted != 0) return false;
+    const int last = kb + t * TK + TK - 1;
+    return last < ke && (last < it.crit_len || it.key_pos(p.crit, last) <= it.qpos0);
+  };
+
+  // ================= pass 1: row statistics =================
+  float pm[MT][2], pl[MT][2];
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ntiles) load_tile(Kg, s, s);
+  for (int mt = 0; mt < MT; ++mt) pm[mt][0] = pm[mt][1] = -INFINITY, pl[mt][0] = pl[mt][1] = 0.f;
+
+#pragma unroll
+  for (int s = 0; s < NSLOT - 1; ++s) {
+    if (s < ntiles) load_tile(Kg, s, ring + s * TILE, keep);
     cp_async_commit();
   }
+  __syncthreads();
   for (int t = 0; t < ntiles; ++t) {
-    cp_async_wait<STAGES - 2>();
+    cp_async_wait<NSLOT - 2>();
     __syncthreads();
     {
-      const int nt = t + STAGES - 1;
-      if (nt < ntiles) load_tile(Kg, nt, nt % STAGES);
+      const int nt = t + NSLOT - 1;
+      if (nt < ntiles) load_tile(Kg, nt, ring + (nt % NSLOT) * TILE, keep);
       cp_async_commit();
     }
-    const __nv_bfloat16* Kt = Kst + (t % STAGES) * TK * KROW;
     float sacc[MT][4];
+    qk_tile<D, MT>(sacc, Qs, ring + (t % NSLOT) * TILE, n0, lane);
+    if (tile_full(t)) {  // every key visible to every row, no planted bias: no per-element checks
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) sacc[mt][0] = sacc[mt][1] = sacc[mt][2] = sacc[mt][3] = 0.f;
-    const int n0 = warp * 8;  // this warp's 8 keys of the tile
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int ks = 0; ks < D / 16; ks += 2) {
-      unsigned b0, b1, b2, b3;
-      ldsm_x4(b0, b1, b2, b3, Kt + (n0 + (lane & 7)) * KROW + ks * 16 + (lane >> 3) * 8);
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        unsigned a0, a1, a2, a3;
-        const __nv_bfloat16* qa = Qs + (mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * KROW + (lane >> 4) * 8;
-        ldsm_x4(a0, a1, a2, a3, qa + ks * 16);
-        mma_bf16(sacc[mt], a0, a1, a2, a3, b0, b1);
-        ldsm_x4(a0, a1, a2, a3, qa + (ks + 1) * 16);
-        mma_bf16(sacc[mt], a0, a1, a2, a3, b2, b3);
-      }
+        for (int hh = 0; hh < 2; ++hh) {
+          const float s0 = sacc[mt][hh * 2] * p.scale_log2, s1 = sacc[mt][hh * 2 + 1] * p.scale_log2;
+          const float nm = fmaxf(pm[mt][hh], fmaxf(s0, s1));
+          pl[mt][hh] = pl[mt][hh] * exp2f(pm[mt][hh] - nm) + exp2f(s0 - nm) + exp2f(s1 - nm);
+          pm[mt][hh] = nm;
+        }
+      continue;
     }
-    // epilogue: scale, causal/extent mask, planted bonus -> S buffer (log2 domain)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int jl = t * TK + n0 + 2 * t4 + e;  // local key index
-      const int gj = kb + jl;
-      const int pos = spos[jl];
-      const bool in_range = gj < ke;
-      const bool is_crit = gj < it.crit_len;
-      const float bias = in_range ? planted_bias(p.planted, p.n_planted, p.bonus_log2, pos) : 0.f;
+      int pos;
+      bool in_range, is_crit;
+      float bias;
+      key_info(t, e, pos, in_range, is_crit, bias);
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int r = mt * 16 + g4 + hh * 8;
-          if (r < R) {
-            const bool vis = in_range && (is_crit || pos <= it.qpos0 + r / G);
-            Sb[r * p.srow + jl] = vis ? fmaf(sacc[mt][hh * 2 + e], p.scale_log2, bias) : -INFINITY;
+          const bool vis = in_range && r < R && (is_crit || pos <= it.qpos0 + r / G);
+          if (vis) {
+            const float s = fmaf(sacc[mt][hh * 2 + e], p.scale_log2, bias);
+            const float nm = fmaxf(pm[mt][hh], s);
+            pl[mt][hh] = pl[mt][hh] * exp2f(pm[mt][hh] - nm) + exp2f(s - nm);
+            pm[mt][hh] = nm;
           }
         }
-      }
     }
   }
   cp_async_wait<0>();
-  __syncthreads();
-
-  // prefetch the first V tiles while the softmax statistics are exchanged
+  // combine the 4 lanes sharing a row, then the 8 warps
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ntiles) load_tile(Vg, s, s);
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      float m = pm[mt][hh], l = pl[mt][hh];
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, m, o);
+        const float ol = __shfl_xor_sync(0xffffffffu, l, o);
+        const float nm = fmaxf(m, om);
+        l = (nm == -INFINITY) ? 0.f : l * exp2f(m - nm) + ol * exp2f(om - nm);
+        m = nm;
+      }
+      if (t4 == 0) {
+        wm[warp * RP + mt * 16 + g4 + hh * 8] = m;
+        wl[warp * RP + mt * 16 + g4 + hh * 8] = l;
+      }
+    }
+  __syncthreads();
+  // prefetch the first K/V pairs of pass 2 while statistics are exchanged
+#pragma unroll
+  for (int s = 0; s < NPAIR - 1; ++s) {
+    if (s < ntiles) {
+      load_tile(Kg, s, ring + (2 * s) * TILE, drop);
+      load_tile(Vg, s, ring + (2 * s + 1) * TILE, drop);
+    }
     cp_async_commit();
   }
-
-  // ---- per-row chunk statistics ----
-  for (int r = warp; r < RP; r += NW) {
+  if (tid < RP) {
     float m = -INFINITY, l = 0.f;
-    if (r < R) {
-      const float* Sr = Sb + r * p.srow;
-      for (int j = lane; j < nk; j += 32) m = fmaxf(m, Sr[j]);
-      m = warp_max(m);
-      if (m != -INFINITY)
-        for (int j = lane; j < nk; j += 32) l += exp2f(Sr[j] - m);
-      l = warp_sum(l);
+    for (int w = 0; w < NW; ++w) {
+      const float om = wm[w * RP + tid], ol = wl[w * RP + tid];
+      const float nm = fmaxf(m, om);
+      l = (nm == -INFINITY) ? 0.f : l * exp2f(m - nm) + ol * exp2f(om - nm);
+      m = nm;
     }
-    if (lane == 0) {
-      rowm[r] = m;
-      rowl[r] = l;
-    }
+    rowm[tid] = m;
+    rowl[tid] = l;
   }
   cluster.sync();
   // ---- exact log-sum-exp over the cluster (DSMEM) ----
@@ -285,12 +347,13 @@ __global__ void __launch_bounds__(NT, 1) attn_mma_kernel(const Params p) {
     }
     rowlse[tid] = lse2;
   }
-  // zero the P-tile padding rows once
-  for (int i = tid; i < (RP - R) * PROW; i += NT) Pt[R * PROW + i] = __float2bfloat16_rn(0.f);
   __syncthreads();
 
-  // ================= phase 2: P, scores, O = P V =================
+  // ================= pass 2: P, scores, O = P V =================
   const bool scores = p.acc != nullptr && it.acc_row >= 0;
+  float lse_r[MT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) lse_r[mt][0] = rowlse[mt * 16 + g4], lse_r[mt][1] = rowlse[mt * 16 + g4 + 8];
   float oacc[MT][NTW][4];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
@@ -298,32 +361,86 @@ __global__ void __launch_bounds__(NT, 1) attn_mma_kernel(const Params p) {
     for (int nt = 0; nt < NTW; ++nt) oacc[mt][nt][0] = oacc[mt][nt][1] = oacc[mt][nt][2] = oacc[mt][nt][3] = 0.f;
 
   for (int t = 0; t < ntiles; ++t) {
-    cp_async_wait<STAGES - 2>();
+    cp_async_wait<NPAIR - 2>();
     __syncthreads();
     {
-      const int nt = t + STAGES - 1;
-      if (nt < ntiles) load_tile(Vg, nt, nt % STAGES);
+      const int nt = t + NPAIR - 1;
+      if (nt < ntiles) {
+        load_tile(Kg, nt, ring + (2 * (nt % NPAIR)) * TILE, drop);
+        load_tile(Vg, nt, ring + (2 * (nt % NPAIR) + 1) * TILE, drop);
+      }
       cp_async_commit();
     }
-    // P tile (bf16) + score emission; thread -> (key, token lane)
-    {
-      const int kk = tid & (TK - 1);
-      const int jl = t * TK + kk;
-      const bool valid = (kb + jl) < ke;
-      for (int qt = tid / TK; qt < it.nq; qt += NT / TK) {
-        float sum = 0.f;
-        for (int g = 0; g < G; ++g) {
-          const int r = qt * G + g;
-          const float pv = valid ? exp2f(Sb[r * p.srow + jl] - rowlse[r]) : 0.f;
-          Pt[r * PROW + kk] = __float2bfloat16_rn(pv);
-          sum += pv;
+    const __nv_bfloat16* Kt = ring + (2 * (t % NPAIR)) * TILE;
+    const __nv_bfloat16* Vt = ring + (2 * (t % NPAIR) + 1) * TILE;
+    float sacc[MT][4];
+    qk_tile<D, MT>(sacc, Qs, Kt, n0, lane);
+    float tok_sum[MT][2][2];  // [mt][hh][e]
+    if (tile_full(t)) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float pv = exp2f(fmaf(sacc[mt][hh * 2 + e], p.scale_log2, -lse_r[mt][hh]));
+            sacc[mt][hh * 2 + e] = pv;
+            tok_sum[mt][hh][e] = pv;
+          }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        int pos;
+        bool in_range, is_crit;
+        float bias;
+        key_info(t, e, pos, in_range, is_crit, bias);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int r = mt * 16 + g4 + hh * 8;
+            const bool vis = in_range && r < R && (is_crit || pos <= it.qpos0 + r / G);
+            const float pv = vis ? exp2f(fmaf(sacc[mt][hh * 2 + e], p.scale_log2, bias) - lse_r[mt][hh]) : 0.f;
+            sacc[mt][hh * 2 + e] = pv;
+            tok_sum[mt][hh][e] = pv;
+          }
+      }
+    }
+    // P tile (bf16, [row][key]) for the PV product
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+        *reinterpret_cast<__nv_bfloat162*>(Pt + (mt * 16 + g4 + hh * 8) * PROW + n0 + 2 * t4) =
+            __floats2bfloat162_rn(sacc[mt][hh * 2], sacc[mt][hh * 2 + 1]);
+    // PillarAttn scores: sum the G rows of each query token (lanes g4 .. g4+G-1)
+    if (scores) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          float v0 = tok_sum[mt][0][e], v1 = tok_sum[mt][1][e];
+          if (G >= 16) v0 += v1;
+          for (int o = 4; o < 4 * min(G, 8); o <<= 1) {
+            v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+            v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+          }
+          const int gj = kb + t * TK + n0 + 2 * t4 + e;
+          if (gj < ke && (g4 % min(G, 8)) == 0) {
+            const int pos = it.key_pos(p.crit, gj);
+            const int tok0 = (mt * 16 + g4) / G;
+            if (v0 != 0.f && tok0 < it.nq)
+              atomicAdd(p.acc + (int64_t)(it.acc_row + tok0 * it.acc_step) * p.acc_stride + pos, v0);
+            if (G < 16) {
+              const int tok1 = (mt * 16 + g4 + 8) / G;
+              if (v1 != 0.f && tok1 < it.nq)
+                atomicAdd(p.acc + (int64_t)(it.acc_row + tok1 * it.acc_step) * p.acc_stride + pos, v1);
+            }
+          }
         }
-        if (scores && sum != 0.f)
-          atomicAdd(p.acc + (int64_t)(it.acc_row + qt * it.acc_step) * p.acc_stride + spos[jl], sum);
       }
     }
     __syncthreads();
-    const __nv_bfloat16* Vt = Kst + (t % STAGES) * TK * KROW;
     const int nb = warp * NCOLW;
 #pragma unroll
     for (int ks = 0; ks < TK / 16; ++ks) {
@@ -347,8 +464,8 @@ __global__ void __launch_bounds__(NT, 1) attn_mma_kernel(const Params p) {
   cp_async_wait<0>();
   __syncthreads();
 
-  // ---- O partial -> smem, cluster reduction through DSMEM ----
-  float* Ob = Sb;  // [RP][D]
+  // ---- O partial -> smem (ring reused), cluster reduction through DSMEM ----
+  float* Ob = reinterpret_cast<float*>(ring);  // [RP][D]
   {
     const int nb = warp * NCOLW;
 #pragma unroll
@@ -387,14 +504,15 @@ __global__ void __launch_bounds__(NT, 1) attn_mma_kernel(const Params p) {
   cluster.sync();
 }
 
-template <int D, int MT>
-int launch_one(const Params& prm, int C, int num_items, int kv_heads, int smem, cudaStream_t stream) {
-  auto kern = attn_mma_kernel<D, MT>;
-  static int configured_smem = 0;
-  if (smem > configured_smem) {
+template <int D, int MT, int NSLOT>
+int launch_one(const Params& prm, int C, int num_items, int kv_heads, cudaStream_t stream) {
+  auto kern = attn_mma_kernel<D, MT, NSLOT>;
+  const int smem = make_layout(D, MT, NSLOT).total;
+  static bool configured = false;
+  if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    configured_smem = smem;
+    configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C, kv_heads, num_items);
@@ -422,35 +540,28 @@ int launch_one(const Params& prm, int C, int num_items, int kv_heads, int smem, 
 bool mma_attn_supported(int dtype, int D, int rows) {
   return dtype == SD_DTYPE_BF16 && (D == 64 || D == 128) && rows >= 1 && rows <= 80;
 }
-static bool plan_mma(int D, int MT, int rows, int max_keys, int num_items, int kv_heads, int* C_out,
-                     int* chunk_out, int* smem_out);
-bool mma_attn_plannable(int dtype, int D, int rows, int max_keys, int num_items, int kv_heads) {
-  if (!mma_attn_supported(dtype, D, rows)) return false;
-  int C, chunk, smem;
-  return plan_mma(D, (rows + 15) / 16, rows, max_keys < 1 ? 1 : max_keys, num_items, kv_heads, &C, &chunk, &smem);
+
+// Cluster size: enough CTAs for ~2 waves of 2 CTAs/SM, chunks of at most
+// ~512 keys so the K re-read of pass 2 stays L2-resident, C <= 16.
+static void plan_mma(int max_keys, int num_items, int kv_heads, int* C_out, int* chunk_out) {
+  using namespace mma_attn;
+  const int tiles = (max_keys + TK - 1) / TK;
+  const int work = num_items * kv_heads;
+  int c = (4 * 148 + work - 1) / work;       // parallelism target
+  const int c_l2 = (tiles + 7) / 8;          // <= 8 tiles (512 keys) per CTA
+  if (c_l2 > c) c = c_l2;
+  if (c > tiles) c = tiles;
+  if (c > 16) c = 16;
+  if (c < 1) c = 1;
+  *C_out = c;
+  *chunk_out = ((tiles + c - 1) / c) * TK;
 }
 
-// Pick cluster size C and chunk so the whole chunk's logits stay in smem.
-static bool plan_mma(int D, int MT, int rows, int max_keys, int num_items, int kv_heads, int* C_out,
-                     int* chunk_out, int* smem_out) {
-  using namespace mma_attn;
-  const int limit = 227 * 1024;
-  const int max_tiles = (max_keys + TK - 1) / TK;
-  int c_par = (2 * 148 + num_items * kv_heads - 1) / (num_items * kv_heads);  // ~2 CTAs per SM
-  c_par = c_par < 1 ? 1 : (c_par > 16 ? 16 : c_par);
-  bool found = false;
-  for (int C = 1; C <= 16; ++C) {
-    int chunk = ((max_tiles + C - 1) / C) * TK;
-    if (chunk < TK) chunk = TK;
-    const Layout L = make_layout(D, MT, chunk, rows);
-    if (L.total > limit) continue;
-    *C_out = C;  // smallest fitting C that also gives enough CTAs (or cannot split further)
-    *chunk_out = chunk;
-    *smem_out = L.total;
-    found = true;
-    if (C >= c_par || C >= max_tiles) break;
-  }
-  return found;
+bool mma_attn_plannable(int dtype, int D, int rows, int max_keys, int num_items, int kv_heads) {
+  (void)max_keys;
+  (void)num_items;
+  (void)kv_heads;
+  return mma_attn_supported(dtype, D, rows);
 }
 
 int launch_attn_mma(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer,
@@ -464,8 +575,8 @@ int launch_attn_mma(const void* q, void* out, float* lse, const sd_paged_kv* kvp
   *handled = false;
   if (!mma_attn_supported(kvp->dtype, D, rows)) return 0;
   const int MT = (rows + 15) / 16;
-  int C = 1, chunk = TK, smem = 0;
-  if (!plan_mma(D, MT, rows, max_keys < 1 ? 1 : max_keys, num_items, kvp->kv_heads, &C, &chunk, &smem)) return 0;
+  int C = 1, chunk = TK;
+  plan_mma(max_keys < 1 ? 1 : max_keys, num_items, kvp->kv_heads, &C, &chunk);
   Params prm;
   prm.q = static_cast<const __nv_bfloat16*>(q);
   prm.out = static_cast<__nv_bfloat16*>(out);
@@ -482,11 +593,9 @@ int launch_attn_mma(const void* q, void* out, float* lse, const sd_paged_kv* kvp
   prm.q_heads = q_heads;
   prm.scale_log2 = scale * LOG2E;
   prm.chunk = chunk;
-  prm.srow = chunk + 8;
-  prm.s_rows = rows;
   *handled = true;
 #define SD_MMA_CASE(DD, M) \
-  if (D == DD && MT == M) return launch_one<DD, M>(prm, C, num_items, kvp->kv_heads, smem, stream);
+  if (D == DD && MT == M) return launch_one<DD, M, 4>(prm, C, num_items, kvp->kv_heads, stream);
   SD_MMA_CASE(128, 1) SD_MMA_CASE(128, 2) SD_MMA_CASE(128, 3) SD_MMA_CASE(128, 4) SD_MMA_CASE(128, 5)
   SD_MMA_CASE(64, 1) SD_MMA_CASE(64, 2) SD_MMA_CASE(64, 3) SD_MMA_CASE(64, 4) SD_MMA_CASE(64, 5)
 #undef SD_MMA_CASE

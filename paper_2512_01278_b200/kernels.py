@@ -102,5 +102,14 @@ def greedy_accept(targets: torch.Tensor, tokens: torch.Tensor, row0: torch.Tenso
             "sd_greedy_accept")
 
 
+def rmsnorm_cast(x: torch.Tensor, out: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:
+    """Glue: RMSNorm without gain of fp32 rows, cast to out.dtype (one launch)."""
+    if x.dtype != torch.float32 or not x.is_contiguous() or not out.is_contiguous():
+        raise ContractError("rmsnorm_cast: x must be contiguous fp32")
+    N.check(N.lib().sd_rmsnorm_cast(x.data_ptr(), x.shape[0], x.shape[1], eps, out.data_ptr(),
+                                    N.dtype_code(out.dtype), N.stream_handle()), "sd_rmsnorm_cast")
+    return out
+
+
 def launch_count() -> int:
     return int(N.lib().sd_launch_count())

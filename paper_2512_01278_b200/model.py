@@ -177,7 +177,7 @@ def plant_attention_concentration(model: ToyModel, positions: Sequence[int], bon
 
 
 def rmsnorm(x: torch.Tensor) -> torch.Tensor:
-    """model.py:225-226 (fp32 statistics)."""
+    """model.py:225-226 (fp32 statistics); torch reference form for tests."""
     return x * torch.rsqrt(torch.mean(x * x, dim=-1, keepdim=True) + RMS_EPS)
 
 
@@ -185,6 +185,25 @@ def _mm(a: torch.Tensor, b: torch.Tensor, out_f32: bool) -> torch.Tensor:
     if a.dtype == torch.float32 or not out_f32:
         return torch.mm(a, b)
     return torch.mm(a, b, out_dtype=torch.float32)
+
+
+_ADDMM_MIXED = None
+
+
+def _residual_add(x: torch.Tensor, a: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """x + a @ w accumulated into the fp32 residual stream in one cuBLAS call
+    (beta = 1) when the torch build supports the mixed-dtype epilogue."""
+    global _ADDMM_MIXED
+    if a.dtype == torch.float32:
+        return x.addmm_(a, w)
+    if _ADDMM_MIXED is not False:
+        try:
+            y = torch.addmm(x, a, w, out_dtype=torch.float32)
+            _ADDMM_MIXED = True
+            return y
+        except (RuntimeError, TypeError):
+            _ADDMM_MIXED = False
+    return x.add_(torch.mm(a, w, out_dtype=torch.float32))
 
 
 @dataclass
@@ -211,16 +230,19 @@ def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_t
     into the pool before attention (K5), so a verify window attends causally to
     its own earlier rows exactly like the reference's token-at-a-time loop
     (model.py:318-340), and a draft row attends to critical U fresh U self
-    (model.py:360-380)."""
+    (model.py:360-380).  Per layer: norm (glue) -> QKV GEMM -> K5 -> K1/K2 ->
+    out-proj GEMM (+residual) -> norm -> MLP-in GEMM -> tanh -> MLP-out GEMM
+    (+residual)."""
     c = model.config
     R = tokens.shape[0]
     Hq, d = c.num_q_heads, c.head_dim
     dt = model.dtype
     x = model.embedding.index_select(0, tokens.long()).float()
+    hn = torch.empty(R, c.hidden_dim, dtype=dt, device=model.device)
     q_buf = torch.empty(R, Hq, d, dtype=dt, device=model.device)
     ctx = torch.empty(R, Hq, d, dtype=dt, device=model.device)
     for l in range(c.num_layers):
-        hn = rmsnorm(x).to(dt)
+        K.rmsnorm_cast(x, hn, RMS_EPS)
         qkv = torch.mm(hn, model.w_qkv[l])
         K.rope_kv_write(qkv, row_table, row_pos, pool, l, Hq, q_buf)
         for ln in launches:
@@ -232,15 +254,18 @@ def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_t
                         planted_bonus=model.planted_bonus, force_generic=force_generic)
             if ln.timer is not None:
                 ln.timer(False)
-        x = x + _mm(ctx.view(R, Hq * d), model.wo[l], True)
-        hm = torch.tanh(_mm(rmsnorm(x).to(dt), model.mlp_in[l], True)).to(dt)
-        x = x + _mm(hm, model.mlp_out[l], True)
+        x = _residual_add(x, ctx.view(R, Hq * d), model.wo[l])
+        K.rmsnorm_cast(x, hn, RMS_EPS)
+        hm = torch.mm(hn, model.mlp_in[l])
+        torch.tanh_(hm)
+        x = _residual_add(x, hm, model.mlp_out[l])
     return x
 
 
 def lm_head(model: ToyModel, x: torch.Tensor) -> torch.Tensor:
     """logits = E . rmsnorm(x) (model.py:339), fp32 output."""
-    return _mm(rmsnorm(x).to(model.dtype), model.embedding.t(), True)
+    hn = K.rmsnorm_cast(x.contiguous(), torch.empty(x.shape, dtype=model.dtype, device=x.device), RMS_EPS)
+    return _mm(hn, model.embedding.t(), True)
 
 
 def make_items(rows: list[tuple], device) -> torch.Tensor:

@@ -186,7 +186,7 @@ __device__ __forceinline__ void qk16(float (&s)[MT][2][4], const __nv_bfloat16* 
 }
 
 template <int D, int MT, int NSLOT>
-__global__ void __launch_bounds__(NT, (MT <= 2 ? 2 : 1)) attn_mma_kernel(const Params p) {
+__global__ void __launch_bounds__(NT, (MT <= 2 && NSLOT <= 4 ? 2 : 1)) attn_mma_kernel(const Params p) {
   constexpr int RP = MT * 16;
   constexpr int KROW = D + 8;
   constexpr int DCH = D / 8;       // 16-byte chunks per key row
@@ -563,13 +563,32 @@ bool mma_attn_supported(int dtype, int D, int rows) {
 
 // Cluster size: enough CTAs for ~4 waves of 2 CTAs/SM, chunks of at most
 // ~512 keys so the K re-read of pass 2 stays L2-resident, C <= 16.
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+// Ring depth (tiles of 64 keys in shared memory): 4 -> two CTAs per SM,
+// 10 -> one CTA per SM with ~9 K tiles / 4 K+V pairs in flight.
+static int ring_slots() {
+  static const int n = env_int("SD_ATTN_NSLOT", 10);
+  return n;
+}
+
+// Cluster size C: enough CTAs for the machine, chunks of at most
+// SD_ATTN_CHUNK_TILES tiles so the K re-read of pass 2 stays L2-resident,
+// C <= 16 (non-portable cluster sizes are enabled); SD_ATTN_C forces C.
 static void plan_mma(int max_keys, int num_items, int kv_heads, int* C_out, int* chunk_out) {
   using namespace mma_attn;
   const int tiles = (max_keys + TK - 1) / TK;
   const int work = num_items * kv_heads;
-  int c = (4 * 148 + work - 1) / work;  // parallelism target
-  const int c_l2 = (tiles + 7) / 8;     // <= 8 tiles (512 keys) per CTA
+  const int per_sm = ring_slots() <= 4 ? 2 : 1;
+  static const int max_chunk_tiles = env_int("SD_ATTN_CHUNK_TILES", 16);
+  static const int force_c = env_int("SD_ATTN_C", 0);
+  int c = (2 * per_sm * 148 + work - 1) / work;  // parallelism target (~2 waves)
+  const int c_l2 = (tiles + max_chunk_tiles - 1) / max_chunk_tiles;
   if (c_l2 > c) c = c_l2;
+  if (force_c > 0) c = force_c;
   if (c > tiles) c = tiles;
   if (c > 16) c = 16;
   if (c < 1) c = 1;
@@ -614,8 +633,12 @@ int launch_attn_mma(const void* q, void* out, float* lse, const sd_paged_kv* kvp
   prm.scale_log2 = scale * LOG2E;
   prm.chunk = chunk;
   *handled = true;
-#define SD_MMA_CASE(DD, M) \
-  if (D == DD && MT == M) return launch_one<DD, M, 4>(prm, C, num_items, kvp->kv_heads, stream);
+  const int nslot = ring_slots();
+#define SD_MMA_CASE(DD, M)                                                                       \
+  if (D == DD && MT == M) {                                                                      \
+    if (nslot <= 4) return launch_one<DD, M, 4>(prm, C, num_items, kvp->kv_heads, stream);       \
+    return launch_one<DD, M, 10>(prm, C, num_items, kvp->kv_heads, stream);                      \
+  }
   SD_MMA_CASE(128, 1) SD_MMA_CASE(128, 2) SD_MMA_CASE(128, 3) SD_MMA_CASE(128, 4) SD_MMA_CASE(128, 5)
   SD_MMA_CASE(64, 1) SD_MMA_CASE(64, 2) SD_MMA_CASE(64, 3) SD_MMA_CASE(64, 4) SD_MMA_CASE(64, 5)
 #undef SD_MMA_CASE

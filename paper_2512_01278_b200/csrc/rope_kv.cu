@@ -4,15 +4,21 @@
 // 326-331, 372-374.  K is stored post-RoPE (drafts gather rotated keys);
 // rows go straight into their paged slot (no per-forward buffer copy,
 // model.py:271-287's _LayerBuffer is eliminated).
+//
+// One CTA per row.  cos/sin of the row's angles are computed once in double
+// (angle = pos * 10000^(-2i/d), exactly as numpy) into shared memory; the
+// (head, pair) rotations are then spread over all threads so consecutive
+// threads touch consecutive elements.  fp32 parity mode rotates in double.
 #include "common.cuh"
 
 namespace sd {
 
 template <typename T>
-__global__ void __launch_bounds__(128) rope_kv_kernel(const T* __restrict__ qkv, int64_t row_stride,
+__global__ void __launch_bounds__(256) rope_kv_kernel(const T* __restrict__ qkv, int64_t row_stride,
                                                       const int32_t* __restrict__ row_table,
                                                       const int32_t* __restrict__ row_pos, PagedKv kv,
                                                       int layer, int q_heads, T* __restrict__ q_out) {
+  extern __shared__ double cs[];  // [half] cos, [half] sin
   const int r = blockIdx.x;
   const int D = kv.head_dim, half = D / 2, Hkv = kv.kv_heads;
   const int pos = row_pos[r];
@@ -21,31 +27,42 @@ __global__ void __launch_bounds__(128) rope_kv_kernel(const T* __restrict__ qkv,
   T* K = static_cast<T*>(const_cast<void*>(kv.k)) + (int64_t)layer * kv.layer_stride;
   T* V = static_cast<T*>(const_cast<void*>(kv.v)) + (int64_t)layer * kv.layer_stride;
   for (int i = threadIdx.x; i < half; i += blockDim.x) {
-    // angle in double exactly as numpy: position * 10000 ** (-(2i)/d)
     const double inv = pow(10000.0, -static_cast<double>(2 * i) / static_cast<double>(D));
     double s, c;
     sincos(static_cast<double>(pos) * inv, &s, &c);
-    for (int hq = 0; hq < q_heads + Hkv; ++hq) {
-      const T* src = x + hq * D;
-      float lo, hi;
-      if constexpr (sizeof(T) == 4) {  // parity mode: rotate in double, round once
-        const double a = to_f(src[i]), b = to_f(src[i + half]);
-        lo = static_cast<float>(a * c - b * s);
-        hi = static_cast<float>(a * s + b * c);
-      } else {
-        const float a = to_f(src[i]), b = to_f(src[i + half]);
-        const float cf = static_cast<float>(c), sf = static_cast<float>(s);
-        lo = a * cf - b * sf;
-        hi = a * sf + b * cf;
-      }
-      T* dst = hq < q_heads ? q_out + ((int64_t)r * q_heads + hq) * D : K + kv.row_off(slot, hq - q_heads);
-      dst[i] = from_f<T>(lo);
-      dst[i + half] = from_f<T>(hi);
+    cs[i] = c;
+    cs[half + i] = s;
+  }
+  __syncthreads();
+  const int pairs = (q_heads + Hkv) * half;
+  for (int idx = threadIdx.x; idx < pairs; idx += blockDim.x) {
+    const int hq = idx / half, i = idx - hq * half;
+    const T* src = x + hq * D;
+    float lo, hi;
+    if constexpr (sizeof(T) == 4) {  // parity mode: rotate in double, round once
+      const double a = to_f(src[i]), b = to_f(src[i + half]);
+      lo = static_cast<float>(a * cs[i] - b * cs[half + i]);
+      hi = static_cast<float>(a * cs[half + i] + b * cs[i]);
+    } else {
+      const float a = to_f(src[i]), b = to_f(src[i + half]);
+      const float cf = static_cast<float>(cs[i]), sf = static_cast<float>(cs[half + i]);
+      lo = a * cf - b * sf;
+      hi = a * sf + b * cf;
     }
+    T* dst = hq < q_heads ? q_out + ((int64_t)r * q_heads + hq) * D : K + kv.row_off(slot, hq - q_heads);
+    dst[i] = from_f<T>(lo);
+    dst[i + half] = from_f<T>(hi);
   }
   const T* vsrc = x + (q_heads + Hkv) * D;
   T* vdst = V + kv.row_off(slot, 0);
-  for (int j = threadIdx.x; j < Hkv * D; j += blockDim.x) vdst[j] = vsrc[j];
+  const int n = Hkv * D;
+  if ((n * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(vsrc) % 16) == 0) {
+    const int nv = n * sizeof(T) / 16;
+    for (int j = threadIdx.x; j < nv; j += blockDim.x)
+      reinterpret_cast<uint4*>(vdst)[j] = reinterpret_cast<const uint4*>(vsrc)[j];
+  } else {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) vdst[j] = vsrc[j];
+  }
 }
 
 }  // namespace sd
@@ -60,13 +77,14 @@ extern "C" int sd_rope_kv_write(const void* qkv, int64_t qkv_row_stride, int32_t
   if (rows == 0) return 0;
   sd::PagedKv p = sd::make_paged(kv);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t smem = sizeof(double) * kv->head_dim;
   if (kv->dtype == SD_DTYPE_F32)
-    sd::rope_kv_kernel<float><<<rows, 128, 0, s>>>(static_cast<const float*>(qkv), qkv_row_stride, row_table,
-                                                  row_pos, p, layer, q_heads, static_cast<float*>(q_out));
+    sd::rope_kv_kernel<float><<<rows, 256, smem, s>>>(static_cast<const float*>(qkv), qkv_row_stride, row_table,
+                                                     row_pos, p, layer, q_heads, static_cast<float*>(q_out));
   else
-    sd::rope_kv_kernel<__nv_bfloat16><<<rows, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(qkv),
-                                                          qkv_row_stride, row_table, row_pos, p, layer,
-                                                          q_heads, static_cast<__nv_bfloat16*>(q_out));
+    sd::rope_kv_kernel<__nv_bfloat16><<<rows, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(qkv),
+                                                             qkv_row_stride, row_table, row_pos, p, layer,
+                                                             q_heads, static_cast<__nv_bfloat16*>(q_out));
   sd::count_launch();
   SD_CUDA_RETURN();
 }

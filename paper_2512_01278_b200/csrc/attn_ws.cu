@@ -128,6 +128,7 @@ struct Params {
   int q_heads;
   float scale_log2;
   int chunk;  // keys per CTA, multiple of TK
+  int nomath; // diagnostics: stream the tiles, skip the math (SD_ATTN_NOMATH=1)
 };
 
 struct Layout {
@@ -353,6 +354,11 @@ __global__ void __launch_bounds__(NT, (MT <= 2 && NSLOT <= 5) ? 2 : 1) attn_ws_k
     for (int t = 0; t < ntiles; ++t) {
       const int s = t % NSLOT;
       mbar_wait(full + s, (t / NSLOT) & 1);
+      if (p.nomath) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+        continue;
+      }
       float sacc[MT][4];
       qk8<D, MT>(sacc, Qs, ring + s * TILE, n0, lane);
       __syncwarp();
@@ -453,6 +459,14 @@ __global__ void __launch_bounds__(NT, (MT <= 2 && NSLOT <= 5) ? 2 : 1) attn_ws_k
     const int fk = ntiles + 2 * t, fv = fk + 1;
     const int sk = fk % NSLOT, sv = fv % NSLOT;
     mbar_wait(full + sk, (fk / NSLOT) & 1);
+    if (p.nomath) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + sk);
+      mbar_wait(full + sv, (fv / NSLOT) & 1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + sv);
+      continue;
+    }
     float sacc[MT][2][4];
     qk16<D, MT>(sacc, Qs, ring + sk * TILE, k0, lane);
     __syncwarp();
@@ -673,6 +687,8 @@ int launch_attn_ws(const void* q, void* out, float* lse, const sd_paged_kv* kvp,
   prm.q_heads = q_heads;
   prm.scale_log2 = scale * LOG2E;
   prm.chunk = chunk;
+  static const int nomath = env_int("SD_ATTN_NOMATH", 0);
+  prm.nomath = nomath;
   *handled = true;
 #define SD_WS_CASE(DD, M)                                                                                    \
   if (D == DD && MT == M) {                                                                                  \

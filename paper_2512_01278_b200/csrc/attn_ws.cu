@@ -72,6 +72,14 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned b
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void cp_async16_pol(void* dst, const void* src, uint64_t policy) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
@@ -129,6 +137,7 @@ struct Params {
   float scale_log2;
   int chunk;  // keys per CTA, multiple of TK
   int nomath; // diagnostics: stream the tiles, skip the math (SD_ATTN_NOMATH=1)
+  int loader; // 0 = cp.async.bulk per key row, 1 = 16-byte cp.async + mbarrier arrive
 };
 
 struct Layout {
@@ -262,7 +271,7 @@ __global__ void __launch_bounds__(NT, (MT <= 2 && NSLOT <= 5) ? 2 : 1) attn_ws_k
 
   // ---- setup (all warps) ----
   if (tid < NSLOT) {
-    mbar_init(full + tid, 1);
+    mbar_init(full + tid, p.loader == 0 ? 1 : 32);
     mbar_init(empty + tid, NCW);
   }
   for (int j = tid; j < ntiles * TK; j += NT) {
@@ -311,14 +320,28 @@ __global__ void __launch_bounds__(NT, (MT <= 2 && NSLOT <= 5) ? 2 : 1) attn_ws_k
         base = (g2 & 1) ? Vg : Kg;
         pol = drop;
       }
-      if (lane == 0) mbar_arrive_tx(full + s, TK * ROWB);
-      __syncwarp();
       __nv_bfloat16* dst = ring + s * TILE;
+      if (p.loader == 0) {
+        // one bulk async copy (TMA engine) per 256-byte key row
+        if (lane == 0) mbar_arrive_tx(full + s, TK * ROWB);
+        __syncwarp();
 #pragma unroll
-      for (int kk = lane; kk < TK; kk += 32) {
-        int j = t * TK + kk;
-        if (j > last_valid) j = last_valid;  // duplicate a valid row; masked by the math warps
-        bulk_copy(dst + kk * KROW, base + (int64_t)sslot[j] * (kvh * D), ROWB, full + s, pol);
+        for (int kk = lane; kk < TK; kk += 32) {
+          int j = t * TK + kk;
+          if (j > last_valid) j = last_valid;  // duplicate a valid row; masked by the math warps
+          bulk_copy(dst + kk * KROW, base + (int64_t)sslot[j] * (kvh * D), ROWB, full + s, pol);
+        }
+      } else {
+        // 16-byte cp.async (LDGSTS), 2 key rows per warp instruction, then an
+        // mbarrier arrive that fires when this lane's copies land
+#pragma unroll 4
+        for (int i = lane; i < TK * DCH; i += 32) {
+          const int kk = i / DCH, c = i - kk * DCH;
+          int j = t * TK + kk;
+          if (j > last_valid) j = last_valid;
+          cp_async16_pol(dst + kk * KROW + c * 8, base + (int64_t)sslot[j] * (kvh * D) + c * 8, pol);
+        }
+        cp_async_mbar_arrive(full + s);
       }
       if (f == ntiles - 1) cluster_arrive();  // pass-1 fills issued: let the exchange proceed
     }
@@ -689,6 +712,8 @@ int launch_attn_ws(const void* q, void* out, float* lse, const sd_paged_kv* kvp,
   prm.chunk = chunk;
   static const int nomath = env_int("SD_ATTN_NOMATH", 0);
   prm.nomath = nomath;
+  static const int loader = env_int("SD_ATTN_LOADER", 0);
+  prm.loader = loader;
   *handled = true;
 #define SD_WS_CASE(DD, M)                                                                                    \
   if (D == DD && MT == M) {                                                                                  \

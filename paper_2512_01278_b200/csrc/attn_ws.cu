@@ -332,14 +332,22 @@ __global__ void __launch_bounds__(NT, (MT <= 2 && NSLOT <= 5) ? 2 : 1) attn_ws_k
           bulk_copy(dst + kk * KROW, base + (int64_t)sslot[j] * (kvh * D), ROWB, full + s, pol);
         }
       } else {
-        // 16-byte cp.async (LDGSTS), 2 key rows per warp instruction, then an
-        // mbarrier arrive that fires when this lane's copies land
-#pragma unroll 4
-        for (int i = lane; i < TK * DCH; i += 32) {
-          const int kk = i / DCH, c = i - kk * DCH;
-          int j = t * TK + kk;
-          if (j > last_valid) j = last_valid;
-          cp_async16_pol(dst + kk * KROW + c * 8, base + (int64_t)sslot[j] * (kvh * D) + c * 8, pol);
+        // 16-byte cp.async (LDGSTS), 32 / DCH key rows per warp instruction
+        // (coalesced), then an mbarrier arrive that fires when this lane's
+        // copies land.  The tile's 64 slots are read once (2 per lane) and
+        // broadcast with shuffles, so no load sits on the issue path.
+        const int j0 = min(t * TK + lane, last_valid), j1 = min(t * TK + lane + 32, last_valid);
+        const int slot0 = sslot[j0], slot1 = sslot[j1];
+        constexpr int KPI = 32 / DCH;  // key rows per warp instruction
+        const int sub = lane / DCH, c = lane - sub * DCH;
+#pragma unroll 8
+        for (int m = 0; m < TK / KPI; ++m) {
+          const int kk = m * KPI + sub;  // key of this lane in instruction m
+          const int src_lane = kk & 31;
+          const int sa = __shfl_sync(0xffffffffu, slot0, src_lane);
+          const int sb = __shfl_sync(0xffffffffu, slot1, src_lane);
+          const int slot = kk < 32 ? sa : sb;
+          cp_async16_pol(dst + kk * KROW + c * 8, base + (int64_t)slot * (kvh * D) + c * 8, pol);
         }
         cp_async_mbar_arrive(full + s);
       }
@@ -712,7 +720,7 @@ int launch_attn_ws(const void* q, void* out, float* lse, const sd_paged_kv* kvp,
   prm.chunk = chunk;
   static const int nomath = env_int("SD_ATTN_NOMATH", 0);
   prm.nomath = nomath;
-  static const int loader = env_int("SD_ATTN_LOADER", 0);
+  static const int loader = env_int("SD_ATTN_LOADER", 1);
   prm.loader = loader;
   *handled = true;
 #define SD_WS_CASE(DD, M)                                                                                    \

@@ -17,6 +17,10 @@ int launch_attn_generic(const void* q, void* out, float* lse, const sd_paged_kv*
                         const int32_t* items, int num_items, int max_keys, int max_nq, const int32_t* crit,
                         float* acc, int64_t acc_stride, const int32_t* planted, int n_planted, float bonus,
                         int q_heads, float scale, void* ws, int64_t ws_bytes, cudaStream_t stream);
+int launch_attn_tm(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer, const int32_t* items,
+                   int num_items, int max_keys, int max_nq, const int32_t* crit, float* acc, int64_t acc_stride,
+                   const int32_t* planted, int n_planted, float bonus, int q_heads, float scale, cudaStream_t stream,
+                   bool* handled);
 int launch_attn_ws(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer, const int32_t* items,
                    int num_items, int max_keys, int max_nq, const int32_t* crit, float* acc, int64_t acc_stride,
                    const int32_t* planted, int n_planted, float bonus, int q_heads, float scale, cudaStream_t stream,
@@ -56,7 +60,15 @@ extern "C" int sd_attention(const void* q, void* out, float* lse, const sd_paged
   if (num_items == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   static const char* impl = getenv("SD_ATTN_IMPL");
+  const bool use_tm = !(impl && (impl[0] == 'm' || impl[0] == 'w'));
   const bool use_ws = !(impl && impl[0] == 'm');
+  if (!(flags & 1) && use_tm) {
+    bool handled = false;
+    const int rc = sd::launch_attn_tm(q, out, lse, kv, layer, items, num_items, max_keys, max_nq, crit, acc,
+                                      acc_row_stride, planted, num_planted, planted_bonus, q_heads, scale, s,
+                                      &handled);
+    if (handled || rc != 0) return rc;
+  }
   if (!(flags & 1) && use_ws) {
     bool handled = false;
     const int rc = sd::launch_attn_ws(q, out, lse, kv, layer, items, num_items, max_keys, max_nq, crit, acc,

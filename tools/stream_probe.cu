@@ -125,7 +125,126 @@ __global__ void k_ws(const uint4* base, int tiles, long long stride_u4, float* o
   if (acc == 1.2345f) out[0] = acc;
 }
 
+// mode 5/6: two passes like the attention kernel: pass 1 streams K (tiles
+// 0..T-1), pass 2 streams K again (L2) and V; mode 6 adds a cluster barrier of
+// C CTAs between the passes.  Producer warp + cp.async + mbarrier, 5 slots.
+template <bool CLUSTER>
+__global__ void k_2pass(const uint4* kbase, const uint4* vbase, int tiles, long long stride_u4, float* out,
+                        int evict) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int NS = 5;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+  uint64_t* empty = full + NS;
+  uint4* ring = reinterpret_cast<uint4*>(smraw + 128);
+  const int unit = blockIdx.x;
+  const uint4* pk = kbase + (long long)unit * tiles * TK * stride_u4;
+  const uint4* pv = vbase + (long long)unit * tiles * TK * stride_u4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < NS) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(full + threadIdx.x)), "r"(32));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(empty + threadIdx.x)), "r"(8));
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n");
+  __syncthreads();
+  auto wait = [&](uint64_t* b, unsigned par) {
+    asm volatile("{\n.reg .pred q;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n@!q bra W_%=;\n}\n" ::"r"(su32(b)), "r"(par));
+  };
+  uint64_t keep, drop;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(keep));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(drop));
+  const int total = 3 * tiles;
+  if (warp == 8) {
+    for (int f = 0; f < total; ++f) {
+      const int s = f % NS;
+      if (f >= NS) wait(empty + s, ((f / NS) - 1) & 1);
+      int t;
+      const uint4* p;
+      uint64_t pol;
+      if (f < tiles) { t = f; p = pk; pol = keep; }
+      else { t = (f - tiles) >> 1; p = ((f - tiles) & 1) ? pv : pk; pol = drop; }
+      uint4* dst = ring + s * 1024;
+#pragma unroll 8
+      for (int c = lane; c < 1024; c += 32) {
+        const int row = c >> 4, part = c & 15;
+        if (evict)
+          asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(su32(dst + c)),
+                       "l"(p + ((long long)(t * TK + row)) * stride_u4 + part), "l"(pol));
+        else
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(dst + c)),
+                       "l"(p + ((long long)(t * TK + row)) * stride_u4 + part));
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(su32(full + s)));
+      if (CLUSTER && f == tiles - 1) asm volatile("barrier.cluster.arrive.release.aligned;\n");
+    }
+    if (CLUSTER) asm volatile("barrier.cluster.wait.acquire.aligned;\n");
+    return;
+  }
+  float acc = 0.f;
+  for (int f = 0; f < total; ++f) {
+    if (CLUSTER && f == tiles) {
+      asm volatile("barrier.cluster.arrive.release.aligned;\n");
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n");
+    }
+    const int s = f % NS;
+    wait(full + s, (f / NS) & 1);
+    acc += __int_as_float(ring[s * 1024 + threadIdx.x].x);
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(empty + s)));
+  }
+  if (CLUSTER && tiles == 0) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n");
+  }
+  if (acc == 1.2345f) out[0] = acc;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 3) {  // two-pass probe: units tiles cluster evict
+    const int units = atoi(argv[1]), tiles = atoi(argv[2]), C = atoi(argv[3]), evict = argc > 4 ? atoi(argv[4]) : 1;
+    const size_t per_unit = (size_t)tiles * TK * STRIDE;
+    void *kb, *vb;
+    float* out;
+    CK(cudaMalloc(&kb, per_unit * units + 4096));
+    CK(cudaMalloc(&vb, per_unit * units + 4096));
+    CK(cudaMalloc(&out, 64));
+    cudaMemset(kb, 1, per_unit * units);
+    cudaMemset(vb, 1, per_unit * units);
+    const int smem = 128 + 5 * 16384;
+    cudaFuncSetAttribute(k_2pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_2pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_2pass<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    auto run = [&]() {
+      if (C <= 0) {
+        k_2pass<false><<<units, 288, smem>>>((const uint4*)kb, (const uint4*)vb, tiles, STRIDE / 16, out, evict);
+      } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(units);
+        cfg.blockDim = dim3(288);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        cfg.attrs = at; cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, k_2pass<true>, (const uint4*)kb, (const uint4*)vb, tiles, (long long)(STRIDE / 16), out, evict));
+      }
+    };
+    run();
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    for (int i = 0; i < 5; ++i) run();
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    ms /= 5;
+    const double hbm = 2.0 * units * tiles * TK * ROWB;
+    printf("2pass units %d tiles %d C %d evict %d: %.1f us  %.0f GB/s (K+V once)\n", units, tiles, C, evict, ms * 1e3,
+           hbm / ms / 1e6);
+    return 0;
+  }
   const int units = argc > 1 ? atoi(argv[1]) : 2048;   // CTAs (one head-stream each)
   const int tiles = argc > 2 ? atoi(argv[2]) : 16;     // 64-row tiles per CTA
   const size_t per_unit = (size_t)tiles * TK * STRIDE;

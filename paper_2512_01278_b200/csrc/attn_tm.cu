@@ -144,6 +144,7 @@ struct Params {
   int q_heads;
   float scale_log2;
   int chunk;  // keys per CTA, multiple of TK, chunk/TK * MT * 4 <= HALF
+  int nomath; // diagnostics: stream only (SD_ATTN_NOMATH=1)
 };
 
 struct Layout {
@@ -228,16 +229,13 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
     mbar_init(full + tid, 32);
     mbar_init(empty + tid, NCW);
   }
+  // key positions only (dense keys: arithmetic; critical keys: one load);
+  // the producer resolves physical slots itself, one tile ahead
   for (int j = tid; j < ntiles * TK; j += NT) {
     const int gj = kb + j;
-    int pos = 0x7fffffff, slot = -1;
-    if (gj < ke) {
-      pos = it.key_pos(p.crit, gj);
-      slot = static_cast<int>(p.kv.slot_of(it.table_row, pos));
-    }
-    spos[j] = pos;
-    sslot[j] = slot;
+    spos[j] = gj < ke ? it.key_pos(p.crit, gj) : 0x7fffffff;
   }
+  (void)sslot;
   for (int i = tid; i < RP * DCH; i += NT) {
     const int r = i / DCH, c = i - r * DCH;
     uint4 v = make_uint4(0, 0, 0, 0);
@@ -262,14 +260,22 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
     const int last_valid = nk - 1;
     constexpr int KPI = 32 / DCH;  // key rows per warp instruction
     const int sub = lane / DCH, c = lane - sub * DCH;
+    // physical slots of tile t's keys (lane, lane+32): block-table loads
+    // issued one fill ahead so their latency overlaps the previous copies
+    auto slots_of = [&](int t, int& s0, int& s1) {
+      s0 = static_cast<int>(p.kv.slot_of(it.table_row, spos[min(t * TK + lane, last_valid)]));
+      s1 = static_cast<int>(p.kv.slot_of(it.table_row, spos[min(t * TK + lane + 32, last_valid)]));
+    };
+    int slot0 = 0, slot1 = 0;
+    if (ntiles > 0) slots_of(0, slot0, slot1);
     for (int f = 0; f < 2 * ntiles; ++f) {
       const int s = f % NSLOT;
-      if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
       const int t = f < ntiles ? f : f - ntiles;
       const __nv_bfloat16* base = f < ntiles ? Kg : Vg;
       __nv_bfloat16* dst = ring + s * TILE;
-      const int slot0 = sslot[min(t * TK + lane, last_valid)];
-      const int slot1 = sslot[min(t * TK + lane + 32, last_valid)];
+      int n0s = 0, n1s = 0;
+      if (f + 1 < 2 * ntiles) slots_of(f + 1 < ntiles ? f + 1 : f + 1 - ntiles, n0s, n1s);
+      if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
 #pragma unroll 8
       for (int m = 0; m < TK / KPI; ++m) {
         const int kk = m * KPI + sub;
@@ -278,6 +284,8 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
         cp_async16_pol(dst + kk * KROW + c * 8, base + (int64_t)(kk < 32 ? sa : sb) * (kvh * D) + c * 8, pol);
       }
       cp_async_mbar_arrive(full + s);
+      slot0 = n0s;
+      slot1 = n1s;
       if (f == ntiles - 1) cluster_arrive();  // K streamed: let the exchange proceed
     }
     if (ntiles == 0) cluster_arrive();
@@ -311,6 +319,11 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
     for (int t = 0; t < ntiles; ++t) {
       const int s = t % NSLOT;
       mbar_wait(full + s, (t / NSLOT) & 1);
+      if (p.nomath) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+        continue;
+      }
       float sacc[MT][4], sb[MT][4];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
@@ -429,6 +442,12 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
   for (int t = 0; t < ntiles; ++t) {
     const int f = ntiles + t;
     const int s = f % NSLOT;
+    if (p.nomath) {
+      mbar_wait(full + s, (f / NSLOT) & 1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+      continue;
+    }
     float P0[MT][4], P1[MT][4];  // keys of warp w4 / of warp w4+4
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
@@ -643,6 +662,8 @@ int launch_attn_tm(const void* q, void* out, float* lse, const sd_paged_kv* kvp,
   prm.q_heads = q_heads;
   prm.scale_log2 = scale * LOG2E;
   prm.chunk = chunk;
+  static const int nomath = env_int("SD_ATTN_NOMATH", 0);
+  prm.nomath = nomath;
   *handled = true;
 #define SD_TM_CASE(DD, M)                                                                   \
   if (D == DD && MT == M) {                                                                 \

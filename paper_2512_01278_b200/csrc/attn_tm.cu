@@ -127,6 +127,14 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr int kTraceCtas = 8192;
+constexpr int kTraceSlots = 8;
+__device__ uint64_t g_trace[kTraceCtas * kTraceSlots];
 
 struct Params {
   const __nv_bfloat16* q;
@@ -145,6 +153,7 @@ struct Params {
   float scale_log2;
   int chunk;  // keys per CTA, multiple of TK, chunk/TK * MT * 4 <= HALF
   int nomath; // diagnostics: stream only (SD_ATTN_NOMATH=1)
+  int trace;  // diagnostics: phase timestamps (SD_ATTN_TRACE=1)
 };
 
 struct Layout {
@@ -203,6 +212,13 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g4 = lane >> 2, t4 = lane & 3;
+  // diagnostics: per-CTA phase timestamps (SD_ATTN_TRACE=1, read with sd_attention_trace)
+  const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#define TRACE(k)                                                                                   \
+  do {                                                                                             \
+    if (p.trace && tid == 0 && cta_lin < kTraceCtas) g_trace[cta_lin * kTraceSlots + (k)] = gtime(); \
+  } while (0)
+  TRACE(0);
 
   extern __shared__ __align__(128) unsigned char smem[];
   const Layout L = make_layout(D, MT, p.chunk);
@@ -249,6 +265,7 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tptr;
+  TRACE(1);
 
   const int kvh = p.kv.kv_heads;
   const __nv_bfloat16* Kg = static_cast<const __nv_bfloat16*>(p.kv.k) + (int64_t)p.layer * p.kv.layer_stride + h * D;
@@ -376,6 +393,7 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
     }
   }
   tmem_wait_st();
+  TRACE(2);
   tc_fence_before();
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
@@ -426,6 +444,7 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
   math_bar();
   tc_fence_after();
 
+  TRACE(3);
   // ---- phase 2: P = exp2(S - lse) from TMEM, scores, O = P V ----
   const int w4 = warp & 3;   // key pair: warps w4 and w4+4 own keys 8*w4.. and 8*w4+32..
   const int dh = warp >> 2;  // output-column half
@@ -527,6 +546,7 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
     if (lane == 0) mbar_arrive(empty + s);
   }
 
+  TRACE(4);
   // ---- O partials: 4 key pairs -> smem (ring reused), cluster DSMEM reduce ----
   math_bar();
   float* Ob = reinterpret_cast<float*>(ring);  // [RP][D]
@@ -565,6 +585,8 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
   cluster_wait();
   tc_fence_after();
   if (warp == 0) tmem_dealloc(tbase, TCOLS);
+  TRACE(5);
+#undef TRACE
 }
 
 template <int D, int MT, bool GM>
@@ -664,6 +686,8 @@ int launch_attn_tm(const void* q, void* out, float* lse, const sd_paged_kv* kvp,
   prm.chunk = chunk;
   static const int nomath = env_int("SD_ATTN_NOMATH", 0);
   prm.nomath = nomath;
+  static const int trace = env_int("SD_ATTN_TRACE", 0);
+  prm.trace = trace;
   *handled = true;
 #define SD_TM_CASE(DD, M)                                                                   \
   if (D == DD && MT == M) {                                                                 \
@@ -678,3 +702,12 @@ int launch_attn_tm(const void* q, void* out, float* lse, const sd_paged_kv* kvp,
 }
 
 }  // namespace sd
+
+// Diagnostics: copy the per-CTA phase timestamps of the last traced launch
+// (SD_ATTN_TRACE=1) to host memory: [ctas][8] uint64 globaltimer ns.
+extern "C" int sd_attention_trace(uint64_t* host_dst, int32_t ctas) {
+  if (ctas > sd::tm_attn::kTraceCtas) ctas = sd::tm_attn::kTraceCtas;
+  cudaError_t e = cudaMemcpyFromSymbol(host_dst, sd::tm_attn::g_trace,
+                                       sizeof(uint64_t) * sd::tm_attn::kTraceSlots * ctas);
+  return e == cudaSuccess ? 0 : (int)e;
+}

@@ -37,9 +37,9 @@ namespace tm_attn {
 constexpr int TK = 64;   // keys per tile
 constexpr int NCW = 8;   // math warps
 constexpr int NT = (NCW + 1) * 32;
-constexpr int NSLOT = 10;
-constexpr int TCOLS = 512;       // TMEM columns per CTA
-constexpr int HALF = TCOLS / 2;  // columns per warp half (warps 0-3 / 4-7)
+// Two shapes: V1 = one CTA per SM (10-slot ring, all 512 TMEM columns);
+// V2 = two CTAs per SM (5-slot ring, 256 columns each) so one CTA's
+// exchange / epilogue bubbles overlap the other's streaming.
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
@@ -159,7 +159,7 @@ struct Params {
 struct Layout {
   int bar_off, tptr_off, ring_off, q_off, pos_off, slot_off, wm_off, wl_off, m_off, l_off, lse_off, total;
 };
-__host__ __device__ inline Layout make_layout(int D, int MT, int chunk) {
+__host__ __device__ inline Layout make_layout(int D, int MT, int chunk, int NSLOT, int TCOLS) {
   const int RP = MT * 16;
   const int krow = D + 8;
   Layout L;
@@ -183,12 +183,13 @@ __host__ __device__ inline Layout make_layout(int D, int MT, int chunk) {
   L.lse_off = o;  o += RP * 4;
   // >= 120 KB keeps occupancy at ONE CTA per SM: each CTA owns all 512 TMEM
   // columns, and two co-resident CTAs of one cluster would deadlock in alloc.
-  L.total = o > 120 * 1024 ? o : 120 * 1024;
+  L.total = (TCOLS == 512 && o < 120 * 1024) ? 120 * 1024 : o;
   return L;
 }
 
-template <int D, int MT, bool GM>
-__global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
+template <int D, int MT, bool GM, int NSLOT, int TCOLS>
+__global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_tm_kernel(const Params p) {
+  constexpr int HALF = TCOLS / 2;  // TMEM columns per warp half (warps 0-3 / 4-7)
   constexpr int RP = MT * 16;
   constexpr int KROW = D + 8;
   constexpr int DCH = D / 8;
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
   TRACE(0);
 
   extern __shared__ __align__(128) unsigned char smem[];
-  const Layout L = make_layout(D, MT, p.chunk);
+  const Layout L = make_layout(D, MT, p.chunk, NSLOT, TCOLS);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* empty = full + NSLOT;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L.tptr_off);
@@ -589,10 +590,10 @@ __global__ void __launch_bounds__(NT, 1) attn_tm_kernel(const Params p) {
 #undef TRACE
 }
 
-template <int D, int MT, bool GM>
+template <int D, int MT, bool GM, int NSLOT, int TCOLS>
 int launch_one(const Params& prm, int C, int num_items, int kv_heads, cudaStream_t stream) {
-  auto kern = attn_tm_kernel<D, MT, GM>;
-  const int smem = make_layout(D, MT, prm.chunk).total;
+  auto kern = attn_tm_kernel<D, MT, GM, NSLOT, TCOLS>;
+  const int smem = make_layout(D, MT, prm.chunk, NSLOT, TCOLS).total;
   static int configured = 0;
   if (smem > configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -629,10 +630,11 @@ static int env_int(const char* name, int dflt) {
 
 // Cluster size: smallest C whose chunk fits the TMEM logit store, then the C
 // (<= 16) that best fills whole waves of 148 single-CTA SMs.
-static bool plan_tm(int max_keys, int num_items, int kv_heads, int MT, int* C_out, int* chunk_out) {
+static bool plan_tm(int max_keys, int num_items, int kv_heads, int MT, int tcols, int* C_out, int* chunk_out) {
   using namespace tm_attn;
   const int tiles = (max_keys + TK - 1) / TK;
-  const int max_tiles = HALF / (MT * 4);
+  const int max_tiles = (tcols / 2) / (MT * 4);
+  const int slots = 148 * (512 / tcols);
   const int c_min = (tiles + max_tiles - 1) / max_tiles;
   if (c_min > 16) return false;
   static const int force_c = env_int("SD_ATTN_C", 0);
@@ -642,7 +644,7 @@ static bool plan_tm(int max_keys, int num_items, int kv_heads, int MT, int* C_ou
   for (int c = c_min; c <= 16 && c <= tiles; ++c) {
     const int chunk_tiles = (tiles + c - 1) / c;
     const double ctas = (double)work * c;
-    const double waves = ctas / 148.0;
+    const double waves = ctas / (double)slots;
     // useful work per wave slot, penalising tiny chunks (fixed per-CTA cost ~1 tile)
     const double eff = (waves / (double)((long long)(waves + 0.999999))) * (chunk_tiles / (chunk_tiles + 1.0));
     if (eff > best_eff + 0.02) best_eff = eff, best = c;
@@ -666,8 +668,13 @@ int launch_attn_tm(const void* q, void* out, float* lse, const sd_paged_kv* kvp,
   const int rows = gm ? 8 * G : max_nq * G;
   if (rows > 80) return 0;
   const int MT = (rows + 15) / 16;
+  static const int variant = env_int("SD_ATTN_TMV", 2);
+  int tcols = variant == 1 ? 512 : 256;
   int C = 1, chunk = TK;
-  if (!plan_tm(max_keys < 1 ? 1 : max_keys, num_items, kvp->kv_heads, MT, &C, &chunk)) return 0;
+  if (!plan_tm(max_keys < 1 ? 1 : max_keys, num_items, kvp->kv_heads, MT, tcols, &C, &chunk)) {
+    if (tcols == 512 || !plan_tm(max_keys < 1 ? 1 : max_keys, num_items, kvp->kv_heads, MT, 512, &C, &chunk)) return 0;
+    tcols = 512;  // long context: fall back to the one-CTA-per-SM shape
+  }
   Params prm;
   prm.q = static_cast<const __nv_bfloat16*>(q);
   prm.out = static_cast<__nv_bfloat16*>(out);
@@ -689,10 +696,14 @@ int launch_attn_tm(const void* q, void* out, float* lse, const sd_paged_kv* kvp,
   static const int trace = env_int("SD_ATTN_TRACE", 0);
   prm.trace = trace;
   *handled = true;
-#define SD_TM_CASE(DD, M)                                                                   \
-  if (D == DD && MT == M) {                                                                 \
-    if (gm) return launch_one<DD, M, true>(prm, C, num_items, kvp->kv_heads, stream);       \
-    return launch_one<DD, M, false>(prm, C, num_items, kvp->kv_heads, stream);              \
+#define SD_TM_CASE(DD, M)                                                                             \
+  if (D == DD && MT == M) {                                                                           \
+    if (tcols == 512) {                                                                               \
+      if (gm) return launch_one<DD, M, true, 10, 512>(prm, C, num_items, kvp->kv_heads, stream);      \
+      return launch_one<DD, M, false, 10, 512>(prm, C, num_items, kvp->kv_heads, stream);             \
+    }                                                                                                 \
+    if (gm) return launch_one<DD, M, true, 5, 256>(prm, C, num_items, kvp->kv_heads, stream);         \
+    return launch_one<DD, M, false, 5, 256>(prm, C, num_items, kvp->kv_heads, stream);                \
   }
   SD_TM_CASE(128, 1) SD_TM_CASE(128, 2) SD_TM_CASE(128, 3) SD_TM_CASE(128, 4) SD_TM_CASE(128, 5)
   SD_TM_CASE(64, 1) SD_TM_CASE(64, 2) SD_TM_CASE(64, 3) SD_TM_CASE(64, 4) SD_TM_CASE(64, 5)

@@ -70,10 +70,9 @@ __global__ void k_cpasync(const uint4* base, int tiles, long long stride_u4, flo
 }
 
 // mode 2/3: producer warp + mbarrier ring
-template <int MODE>
+template <int MODE, int NS = 5, int NPROD = 1>
 __global__ void k_ws(const uint4* base, int tiles, long long stride_u4, float* out) {
   extern __shared__ __align__(128) unsigned char smraw[];
-  constexpr int NS = 5;
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   uint64_t* empty = full + NS;
   uint4* ring = reinterpret_cast<uint4*>(smraw + 128);
@@ -81,7 +80,7 @@ __global__ void k_ws(const uint4* base, int tiles, long long stride_u4, float* o
   const uint4* p = base + (long long)unit * tiles * TK * stride_u4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < NS) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(full + threadIdx.x)), "r"(MODE == 2 ? 32 : 1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(full + threadIdx.x)), "r"(MODE == 2 ? 32 * NPROD : 1));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(empty + threadIdx.x)), "r"(8));
   }
   asm volatile("fence.mbarrier_init.release.cluster;\n");
@@ -89,20 +88,21 @@ __global__ void k_ws(const uint4* base, int tiles, long long stride_u4, float* o
   auto wait = [&](uint64_t* b, unsigned par) {
     asm volatile("{\n.reg .pred q;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n@!q bra W_%=;\n}\n" ::"r"(su32(b)), "r"(par));
   };
-  if (warp == 8) {
+  if (warp >= 8) {
+    const int pw = warp - 8;
     for (int t = 0; t < tiles; ++t) {
       const int s = t % NS;
       if (t >= NS) wait(empty + s, ((t / NS) - 1) & 1);
       uint4* dst = ring + s * 1024;
       if (MODE == 2) {
 #pragma unroll 8
-        for (int c = lane; c < 1024; c += 32) {
+        for (int c = lane + 32 * pw; c < 1024; c += 32 * NPROD) {
           const int row = c >> 4, part = c & 15;
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(dst + c)),
                        "l"(p + ((long long)(t * TK + row)) * stride_u4 + part));
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(su32(full + s)));
-      } else {
+      } else if (pw == 0) {
         if (lane == 0)
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(full + s)), "r"(TK * ROWB));
         __syncwarp();
@@ -258,7 +258,8 @@ int main(int argc, char** argv) {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const double useful = (double)units * tiles * TK * ROWB;
-  for (int mode = 0; mode <= 4; ++mode) {
+  for (int mode = 0; mode <= 8; ++mode) {
+    if (mode == 5 || mode == 6) continue;
     long long stride_u4 = (mode == 4) ? ROWB / 16 : STRIDE / 16;
     auto run = [&]() {
       if (mode == 0 || mode == 4) k_ldg<<<units, 256>>>((const uint4*)buf, tiles, stride_u4, out);
@@ -268,6 +269,11 @@ int main(int argc, char** argv) {
                        k_ws<2><<<units, 288, 128 + 5 * 16384>>>((const uint4*)buf, tiles, stride_u4, out); }
       if (mode == 3) { cudaFuncSetAttribute(k_ws<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 + 5 * 16384);
                        k_ws<3><<<units, 288, 128 + 5 * 16384>>>((const uint4*)buf, tiles, stride_u4, out); }
+      if (mode == 5 || mode == 6) return;  // (two-pass modes use the other entry)
+      if (mode == 7) { auto k = k_ws<2, 10, 1>; cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 + 12 * 16384);
+                       k<<<units, 288, 128 + 12 * 16384>>>((const uint4*)buf, tiles, stride_u4, out); }
+      if (mode == 8) { auto k = k_ws<2, 10, 2>; cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 + 12 * 16384);
+                       k<<<units, 320, 128 + 12 * 16384>>>((const uint4*)buf, tiles, stride_u4, out); }
     };
     run();
     CK(cudaDeviceSynchronize());

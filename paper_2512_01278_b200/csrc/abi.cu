@@ -21,6 +21,10 @@ int launch_attn_tm(const void* q, void* out, float* lse, const sd_paged_kv* kvp,
                    int num_items, int max_keys, int max_nq, const int32_t* crit, float* acc, int64_t acc_stride,
                    const int32_t* planted, int n_planted, float bonus, int q_heads, float scale, cudaStream_t stream,
                    bool* handled);
+int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer, const int32_t* items,
+                     int num_items, int max_keys, int max_nq, const int32_t* crit, float* acc, int64_t acc_stride,
+                     const int32_t* planted, int n_planted, float bonus, int q_heads, float scale,
+                     cudaStream_t stream, bool* handled);
 int launch_attn_ws(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer, const int32_t* items,
                    int num_items, int max_keys, int max_nq, const int32_t* crit, float* acc, int64_t acc_stride,
                    const int32_t* planted, int n_planted, float bonus, int q_heads, float scale, cudaStream_t stream,
@@ -59,9 +63,20 @@ extern "C" int sd_attention(const void* q, void* out, float* lse, const sd_paged
   SD_REQUIRE(num_planted == 0 || planted != nullptr, "sd_attention: planted list missing");
   if (num_items == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // SD_ATTN_IMPL (diagnostics): u = tcgen05 kernel first (default), t = TMEM-logit
+  // mma.sync kernel, w = warp-specialized mma.sync, m = two-pass mma.sync
   static const char* impl = getenv("SD_ATTN_IMPL");
-  const bool use_tm = !(impl && (impl[0] == 'm' || impl[0] == 'w'));
-  const bool use_ws = !(impl && impl[0] == 'm');
+  const char sel = impl && impl[0] ? impl[0] : 'u';
+  const bool use_umma = sel == 'u';
+  const bool use_tm = sel == 'u' || sel == 't';
+  const bool use_ws = sel != 'm';
+  if (!(flags & 1) && use_umma) {
+    bool handled = false;
+    const int rc = sd::launch_attn_umma(q, out, lse, kv, layer, items, num_items, max_keys, max_nq, crit, acc,
+                                        acc_row_stride, planted, num_planted, planted_bonus, q_heads, scale, s,
+                                        &handled);
+    if (handled || rc != 0) return rc;
+  }
   if (!(flags & 1) && use_tm) {
     bool handled = false;
     const int rc = sd::launch_attn_tm(q, out, lse, kv, layer, items, num_items, max_keys, max_nq, crit, acc,

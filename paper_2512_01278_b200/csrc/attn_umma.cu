@@ -1,0 +1,648 @@
+// tcgen05 (UMMA) paged attention for sm_100a: K2 verify with PillarAttn score
+// emission and K1 sparse draft, every K and V row read from HBM exactly once.
+//
+// Orientation ("swap AB"): the KEYS of a 128-key tile are the UMMA M dimension
+// and the item's query rows (token x GQA group, padded to NR) are N:
+//
+//   S^T[128 keys][NR] = K_tile[128][d] . Q^T            (kind::f16, K = d)
+//   O^T[d][NR]       += V_tile^T[d][128] . P^T[128][NR]  (A MN-major, K = keys)
+//
+// so TMEM lane = key (phase 1/2) and lane = head-dim column (epilogue): each
+// softmax thread owns ONE key and holds all NR query-row logits of it in
+// registers.  Consequences:
+//   * per-row online (max, sum) is thread-local across tiles; the cross-key
+//     reduction happens once per CTA (shuffles + smem + DSMEM across the
+//     cluster), not once per tile;
+//   * the PillarAttn score  acc[token][pos] += sum_g exp(s - lse)  is a
+//     register-local sum over the G group columns: one RED per (key, token);
+//   * the planted bonus and the causal mask are per-key scalars.
+//
+// The logits of the CTA's whole key chunk stay in TMEM between the passes
+// (up to TMAX tiles of NR fp32 columns), so the exact lse is known before
+// any probability is formed (SURVEY.md §7.2 option (c)) without re-reading K.
+//
+//   grid = (C, kv_heads, items), cluster (C,1,1): CTA c owns keys
+//   [c*chunk, (c+1)*chunk) of the item's key list (critical list, then the
+//   dense causal range).
+//   warps 0-3  softmax / scores / P^T -> smem / epilogue (TMEM lanes 0..127)
+//   warp 4     producer: 16-byte cp.async of 256-byte key rows (paged gather)
+//              into an NSLOT x 32 KB ring in the UMMA SWIZZLE_128B layout;
+//              K tiles of the chunk, then V tiles (each row once)
+//   warp 5     TMEM allocator + single-thread tcgen05.mma issuer
+//
+// Restates model.py:229-253 (_attend) for forward_full (model.py:318-334) and
+// forward_sparse (model.py:360-380), and the score path selection.py:78-135.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace sd {
+namespace umma_attn {
+
+constexpr int TK = 128;                 // keys per tile = UMMA M
+constexpr int D = 128;                  // head dim (two 64-element swizzle atoms)
+constexpr int NSW = 4;                  // softmax warps
+constexpr int WPROD = 4, WMMA = 5;
+constexpr int NT = 6 * 32;
+constexpr int TILE_BYTES = TK * D * 2;  // 32 KB
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t policy) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void sw_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NSW * 32) : "memory"); }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void red_add(float* p, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;\n" ::"l"(p), "f"(v) : "memory");
+}
+
+// ---- tensor memory / UMMA ----
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, int cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst)), "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, int cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(cols));
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// 16 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <int NR>
+__device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&v)[NR]) {
+#pragma unroll
+  for (int c = 0; c < NR; c += 16) tmem_ld16(taddr + c, v + c);
+  tmem_wait_ld();
+}
+
+// SM100 shared-memory matrix descriptor (start, LBO, SBO in 16-byte units,
+// version 1, layout type in bits 61-63: 0 = no swizzle, 2 = 128-byte swizzle)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
+}
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32, M = 128, N = n
+__device__ __forceinline__ uint32_t idesc_bf16(int n, bool a_mn_major, bool b_mn_major) {
+  return (1u << 4)                        // D format f32
+         | (1u << 7) | (1u << 10)         // A, B format bf16
+         | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+struct Params {
+  const __nv_bfloat16* q;
+  __nv_bfloat16* out;
+  float* lse_out;
+  PagedKv kv;
+  int layer;
+  const int32_t* items;
+  const int32_t* crit;
+  float* acc;
+  int64_t acc_stride;
+  const int32_t* planted;
+  int n_planted;
+  float bonus_log2;
+  int q_heads;
+  float scale_log2;
+  int chunk;  // keys per CTA, multiple of TK
+};
+
+struct Layout {
+  int ring, q, pbuf, pos, bar, wm, wl, rowm, rowl, rowlse, tptr, total;
+};
+__host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
+__host__ __device__ inline Layout make_layout(int NR, int NSLOT, int TMAX) {
+  Layout L{};
+  int o = 0;
+  L.ring = o;  o += NSLOT * TILE_BYTES;
+  L.q = o;     o += 2 * NR * 128;        // [dhalf][NR][128 B], SWIZZLE_128B
+  L.pbuf = o;  o += 2 * NR * TK * 2;     // 2 x P^T [128 keys][NR] bf16, MN-major, no swizzle
+  L.pos = o;   o += TMAX * TK * 4;
+  o = align_up(o, 8);
+  L.bar = o;   o += (2 * NSLOT + TMAX + 5) * 8;
+  L.wm = o;    o += NSW * NR * 4;
+  L.wl = o;    o += NSW * NR * 4;
+  L.rowm = o;  o += NR * 4;
+  L.rowl = o;  o += NR * 4;
+  L.rowlse = o; o += NR * 4;
+  L.tptr = o;  o += 16;
+  L.total = align_up(o, 1024) + 1024;  // + slack to 1024-align the dynamic base
+  return L;
+}
+
+template <int G, int NR, int NSLOT, int TCOLS>
+__global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(const Params p) {
+  constexpr int TMAX = (TCOLS - NR) / NR;  // S tiles resident in TMEM
+  constexpr int OCOL = TMAX * NR;          // O^T accumulator columns
+  constexpr int NTOK = NR / G;             // token slots covered by NR rows
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = static_cast<int>(cluster.num_blocks());
+  const int crank = static_cast<int>(cluster.block_rank());
+  const int h = blockIdx.y;
+  const Item it = load_item(p.items, blockIdx.z);
+  const int R = it.nq * G;
+  const int Nk = it.num_keys();
+  const int kb = crank * p.chunk;
+  const int ke = min(Nk, kb + p.chunk);
+  const int nk = max(0, ke - kb);
+  const int ntiles = (nk + TK - 1) / TK;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const Layout L = make_layout(NR, NSLOT, TMAX);
+  unsigned char* ring = smem + L.ring;
+  unsigned char* qs = smem + L.q;
+  unsigned char* pbuf = smem + L.pbuf;
+  int32_t* spos = reinterpret_cast<int32_t*>(smem + L.pos);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);
+  uint64_t* empty = full + NSLOT;
+  uint64_t* sbar = empty + NSLOT;        // [TMAX] S tile t in TMEM
+  uint64_t* pready = sbar + TMAX;        // [2] P^T buffer written
+  uint64_t* pfree = pready + 2;          // [2] P^T buffer consumed by the PV MMA
+  uint64_t* obar = pfree + 2;            // O^T complete
+  float* wm = reinterpret_cast<float*>(smem + L.wm);
+  float* wl = reinterpret_cast<float*>(smem + L.wl);
+  float* rowm = reinterpret_cast<float*>(smem + L.rowm);
+  float* rowl = reinterpret_cast<float*>(smem + L.rowl);
+  float* rowlse = reinterpret_cast<float*>(smem + L.rowlse);
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L.tptr);
+
+  // ---- setup ----
+  if (warp == WMMA) tmem_alloc(tptr, TCOLS);
+  if (tid == 0) {
+    for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, 32), mbar_init(empty + i, 1);
+    for (int i = 0; i < TMAX; ++i) mbar_init(sbar + i, 1);
+    mbar_init(pready + 0, NSW * 32), mbar_init(pready + 1, NSW * 32);
+    mbar_init(pfree + 0, 1), mbar_init(pfree + 1, 1);
+    mbar_init(obar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int j = tid; j < ntiles * TK; j += NT) {
+    const int gj = kb + j;
+    spos[j] = gj < ke ? it.key_pos(p.crit, gj) : -1;
+  }
+  // Q rows (token-major: r = tok*G + g) -> [dhalf][NR][128 B] SWIZZLE_128B, zero padding rows
+  for (int i = tid; i < NR * 16; i += NT) {
+    const int r = i >> 4, c = i & 15;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < R)
+      v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)(it.q_row0 + r / G) * p.q_heads + h * G + r % G) * D +
+                                          c * 8);
+    *reinterpret_cast<uint4*>(qs + (c >> 3) * (NR * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tptr;
+
+  const int64_t row_stride = (int64_t)p.kv.kv_heads * D;  // elements between consecutive slots
+  const __nv_bfloat16* Kg = static_cast<const __nv_bfloat16*>(p.kv.k) + (int64_t)p.layer * p.kv.layer_stride + h * D;
+  const __nv_bfloat16* Vg = static_cast<const __nv_bfloat16*>(p.kv.v) + (int64_t)p.layer * p.kv.layer_stride + h * D;
+
+  if (warp == WPROD) {
+    // ===================== producer =====================
+    const uint64_t pol = policy_evict_first();  // every row is read exactly once
+    const int sub = lane >> 4, c = lane & 15;   // 2 key rows x 16 chunks per instruction
+    const uint32_t ring_u = smem_u32(ring);
+    const int last = nk - 1;
+    int sl[4], nsl[4];
+    auto resolve = [&](int t, int (&s)[4]) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int j = min(t * TK + m * 32 + lane, last);
+        s[m] = static_cast<int>(p.kv.slot_of(it.table_row, spos[j]));
+      }
+    };
+    if (ntiles > 0) resolve(0, sl);
+    for (int f = 0; f < 2 * ntiles; ++f) {
+      const int s = f % NSLOT;
+      const __nv_bfloat16* base = (f < ntiles ? Kg : Vg) + c * 8;
+      if (f + 1 < 2 * ntiles) resolve(f + 1 < ntiles ? f + 1 : f + 1 - ntiles, nsl);
+      if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
+      const uint32_t dst0 = ring_u + s * TILE_BYTES + (c >> 3) * (TK * 128);
+#pragma unroll
+      for (int kk = 0; kk < TK / 2; ++kk) {
+        const int i = 2 * kk + sub;  // key row within the tile
+        const int slot = __shfl_sync(0xffffffffu, sl[kk >> 4], i & 31);
+        cp_async16(dst0 + i * 128 + (((c & 7) ^ (i & 7)) << 4), base + (int64_t)slot * row_stride, pol);
+      }
+      cp_async_mbar_arrive(full + s);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) sl[m] = nsl[m];
+      if (f == ntiles - 1) cluster_arrive();  // K streamed; let the exchange proceed
+    }
+    if (ntiles == 0) cluster_arrive();
+    cluster_wait();
+    cluster_arrive();
+    cluster_wait();
+    cluster_arrive();
+    cluster_wait();
+    return;
+  }
+
+  if (warp == WMMA) {
+    // ===================== MMA issuer =====================
+    const uint32_t ring_u = smem_u32(ring), q_u = smem_u32(qs), p_u = smem_u32(pbuf);
+    const uint32_t id_qk = idesc_bf16(NR, false, false);
+    const uint32_t id_pv = idesc_bf16(NR, true, true);
+    const bool leader = lane == 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int s = t % NSLOT;
+      mbar_wait(full + s, (t / NSLOT) & 1);
+      fence_proxy_async();
+      tc_fence_after();
+      if (leader) {
+        const uint32_t a0 = ring_u + s * TILE_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t off = (ks & 3) << 5;  // K = 16 bf16 = 32 B steps inside the 128-B atom
+          const uint64_t a = smem_desc(a0 + (ks >> 2) * (TK * 128) + off, 16, 1024, 2);
+          const uint64_t b = smem_desc(q_u + (ks >> 2) * (NR * 128) + off, 16, 1024, 2);
+          umma(tbase + t * NR, a, b, id_qk, ks > 0);
+        }
+        umma_commit(empty + s);
+        umma_commit(sbar + t);
+      }
+      __syncwarp();
+    }
+    cluster_arrive();  // barrier 1: this warp's part of phase 1 is issued
+    for (int t = 0; t < ntiles; ++t) {
+      const int f = ntiles + t;
+      const int s = f % NSLOT;
+      mbar_wait(full + s, (f / NSLOT) & 1);
+      mbar_wait(pready + (t & 1), (t >> 1) & 1);
+      fence_proxy_async();
+      tc_fence_after();
+      if (leader) {
+        const uint32_t a0 = ring_u + s * TILE_BYTES;
+        const uint32_t b0 = p_u + (t & 1) * (NR * TK * 2);
+#pragma unroll
+        for (int ks = 0; ks < TK / 16; ++ks) {
+          // A = V^T: MN-major SW128, 64-d atoms LBO = 16 KB apart, 8-key groups SBO = 1 KB
+          const uint64_t a = smem_desc(a0 + ks * 16 * 128, TK * 128, 1024, 2);
+          // B = P^T: MN-major no swizzle, 8-key core groups LBO = 128 B, 8-row groups SBO = 2 KB
+          const uint64_t b = smem_desc(b0 + ks * 2 * 128, 128, TK * 16, 0);
+          umma(tbase + OCOL, a, b, id_pv, (t > 0 || ks > 0) ? 1u : 0u);
+        }
+        umma_commit(empty + s);
+        umma_commit(pfree + (t & 1));
+        if (t == ntiles - 1) umma_commit(obar);
+      }
+      __syncwarp();
+    }
+    cluster_wait();
+    cluster_arrive();
+    cluster_wait();
+    cluster_arrive();
+    cluster_wait();
+    tc_fence_after();
+    tmem_dealloc(tbase, TCOLS);
+    return;
+  }
+
+  // ===================== softmax warps (TMEM lane = key) =====================
+  const int kl = warp * 32 + lane;                  // key (and later d) index within the tile
+  const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
+  float m[NR], l[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) m[r] = -INFINITY, l[r] = 0.f;
+
+  // per-key scalars for tile t: bias and first visible row (rows >= rmin see the key)
+  auto key_info = [&](int t, int& pos, float& bias, int& rmin) {
+    const int j = t * TK + kl;
+    pos = spos[j];
+    const int gj = kb + j;
+    if (pos < 0) {
+      rmin = NR;  // past the chunk: invisible to every row
+      bias = 0.f;
+      return;
+    }
+    rmin = gj < it.crit_len ? 0 : max(0, pos - it.qpos0) * G;
+    bias = p.n_planted ? planted_bias(p.planted, p.n_planted, p.bonus_log2, pos) : 0.f;
+  };
+
+  // ---- phase 1: S^T tiles -> thread-local online (max, sum) ----
+  for (int t = 0; t < ntiles; ++t) {
+    int pos, rmin;
+    float bias;
+    key_info(t, pos, bias, rmin);
+    mbar_wait(sbar + t, 0);
+    tc_fence_after();
+    float v[NR];
+    tmem_ld_row<NR>(tl + t * NR, v);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      if (r >= rmin && r < R) {
+        const float s2 = fmaf(v[r], p.scale_log2, bias);
+        const float nm = fmaxf(m[r], s2);
+        l[r] = l[r] * ex2(m[r] - nm) + ex2(s2 - nm);
+        m[r] = nm;
+      }
+    }
+  }
+  // ---- exchange: warp -> CTA -> cluster row statistics -> exact lse ----
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    if (r < R) {
+      float mw = m[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+      float lw = (mw == -INFINITY) ? 0.f : l[r] * ex2(m[r] - mw);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, o);
+      if (lane == 0) wm[warp * NR + r] = mw, wl[warp * NR + r] = lw;
+    }
+  }
+  sw_bar();
+  if (tid < R) {
+    float mm = -INFINITY, ll = 0.f;
+#pragma unroll
+    for (int w = 0; w < NSW; ++w) {
+      const float om = wm[w * NR + tid], ol = wl[w * NR + tid];
+      const float nm = fmaxf(mm, om);
+      ll = (nm == -INFINITY) ? 0.f : ll * ex2(mm - nm) + ol * ex2(om - nm);
+      mm = nm;
+    }
+    rowm[tid] = mm;
+    rowl[tid] = ll;
+  }
+  cluster_arrive();
+  cluster_wait();
+  if (tid < NR) {
+    float lse2 = INFINITY;  // padding rows -> P = 0
+    if (tid < R) {
+      float M = -INFINITY;
+      for (int c = 0; c < C; ++c) M = fmaxf(M, *cluster.map_shared_rank(rowm + tid, c));
+      float Ls = 0.f;
+      for (int c = 0; c < C; ++c) {
+        const float mc = *cluster.map_shared_rank(rowm + tid, c);
+        if (mc != -INFINITY) Ls += *cluster.map_shared_rank(rowl + tid, c) * ex2(mc - M);
+      }
+      lse2 = M + log2f(Ls);
+    }
+    rowlse[tid] = lse2;
+  }
+  sw_bar();
+  float lse[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) lse[r] = rowlse[r];
+
+  // ---- phase 2: P = exp2(S - lse) (final), scores, P^T -> smem for the PV MMA ----
+  const bool scores = p.acc != nullptr && it.acc_row >= 0;
+  for (int t = 0; t < ntiles; ++t) {
+    int pos, rmin;
+    float bias;
+    key_info(t, pos, bias, rmin);
+    float v[NR];
+    tmem_ld_row<NR>(tl + t * NR, v);
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+      v[r] = (r >= rmin && r < R) ? ex2(fmaf(v[r], p.scale_log2, bias) - lse[r]) : 0.f;
+    if (scores && rmin < R) {
+      if (it.acc_step == 0) {
+        float sum = 0.f;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) sum += v[r];
+        if (sum != 0.f) red_add(p.acc + (int64_t)it.acc_row * p.acc_stride + pos, sum);
+      } else {
+#pragma unroll
+        for (int tk = 0; tk < NTOK; ++tk) {
+          float sum = 0.f;
+#pragma unroll
+          for (int g = 0; g < G; ++g) sum += v[tk * G + g];
+          if (sum != 0.f)
+            red_add(p.acc + (int64_t)(it.acc_row + tk * it.acc_step) * p.acc_stride + pos, sum);
+        }
+      }
+    }
+    if (t >= 2) mbar_wait(pfree + (t & 1), ((t >> 1) - 1) & 1);
+    // P^T [key][row]: core matrix (8 keys x 8 rows) = 128 B; key groups 128 B apart,
+    // row groups TK*16 B apart -> this thread's 8-row chunks at kl*16 + ng*TK*16
+    unsigned char* pb = pbuf + (t & 1) * (NR * TK * 2) + kl * 16;
+#pragma unroll
+    for (int ng = 0; ng < NR / 8; ++ng) {
+      __nv_bfloat162 b0 = __floats2bfloat162_rn(v[ng * 8 + 0], v[ng * 8 + 1]);
+      __nv_bfloat162 b1 = __floats2bfloat162_rn(v[ng * 8 + 2], v[ng * 8 + 3]);
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(v[ng * 8 + 4], v[ng * 8 + 5]);
+      __nv_bfloat162 b3 = __floats2bfloat162_rn(v[ng * 8 + 6], v[ng * 8 + 7]);
+      uint4 u;
+      u.x = *reinterpret_cast<uint32_t*>(&b0);
+      u.y = *reinterpret_cast<uint32_t*>(&b1);
+      u.z = *reinterpret_cast<uint32_t*>(&b2);
+      u.w = *reinterpret_cast<uint32_t*>(&b3);
+      *reinterpret_cast<uint4*>(pb + ng * TK * 16) = u;
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    mbar_arrive(pready + (t & 1));
+  }
+
+  // ---- epilogue: O^T (lane = d) -> cluster reduction -> out ----
+  float o[NR];
+  if (ntiles > 0) {
+    mbar_wait(obar, 0);
+    tc_fence_after();
+    tmem_ld_row<NR>(tl + OCOL, o);
+  } else {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) o[r] = 0.f;
+  }
+  const int dcol = kl;
+  if (C == 1) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+      if (r < R)
+        p.out[((int64_t)(it.q_row0 + r / G) * p.q_heads + h * G + r % G) * D + dcol] = __float2bfloat16_rn(o[r]);
+    cluster_arrive();
+    cluster_wait();
+  } else {
+    // all MMAs of this CTA are complete (obar): the ring is free for the O^T partial
+    float* Ob = reinterpret_cast<float*>(ring);  // [NR][D]
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+      if (r < R) Ob[r * D + dcol] = o[r];
+    cluster_arrive();
+    cluster_wait();
+    for (int r = crank; r < R; r += C) {
+      float sum = 0.f;
+      for (int c = 0; c < C; ++c) sum += *cluster.map_shared_rank(Ob + r * D + dcol, c);
+      p.out[((int64_t)(it.q_row0 + r / G) * p.q_heads + h * G + r % G) * D + dcol] = __float2bfloat16_rn(sum);
+    }
+  }
+  if (p.lse_out != nullptr && crank == 0 && tid < R)
+    p.lse_out[(int64_t)(it.q_row0 + tid / G) * p.q_heads + h * G + tid % G] = rowlse[tid] * LN2;
+  tc_fence_before();
+  cluster_arrive();
+  cluster_wait();
+}
+
+template <int G, int NR, int NSLOT, int TCOLS>
+int launch_one(const Params& prm, int C, int num_items, int kv_heads, cudaStream_t stream) {
+  constexpr int TMAX = (TCOLS - NR) / NR;
+  auto kern = attn_umma_kernel<G, NR, NSLOT, TCOLS>;
+  const int smem = make_layout(NR, NSLOT, TMAX).total;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, kv_heads, num_items);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm);
+  count_launch();
+  if (e != cudaSuccess) {
+    set_error(std::string("sd_attention (umma) launch: ") + cudaGetErrorString(e));
+    return (int)e;
+  }
+  return 0;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+}  // namespace umma_attn
+
+// Cluster size: smallest C whose chunk fits the TMEM logit store (TMAX tiles),
+// then the C (<= 16) that best fills whole waves of the SM slots.
+static bool plan_umma(int max_keys, int num_items, int kv_heads, int tmax, int slots, int* C_out, int* chunk_out) {
+  using namespace umma_attn;
+  const int tiles = (max_keys + TK - 1) / TK;
+  const int c_min = (tiles + tmax - 1) / tmax;
+  if (c_min > 16) return false;
+  static const int force_c = env_int("SD_ATTN_C", 0);
+  const int work = num_items * kv_heads;
+  int best = c_min;
+  double best_eff = -1.0;
+  for (int c = c_min; c <= 16 && c <= tiles; ++c) {
+    const int chunk_tiles = (tiles + c - 1) / c;
+    const double waves = (double)work * c / (double)slots;
+    // whole-wave fill x amortisation of the fixed per-CTA cost (~1 tile)
+    const double eff = (waves / (double)((long long)(waves + 0.999999))) * (chunk_tiles / (chunk_tiles + 1.0));
+    if (eff > best_eff + 0.02) best_eff = eff, best = c;
+  }
+  if (force_c >= c_min && force_c <= 16) best = force_c;
+  *C_out = best;
+  *chunk_out = ((tiles + best - 1) / best) * TK;
+  return true;
+}
+
+int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer, const int32_t* items,
+                     int num_items, int max_keys, int max_nq, const int32_t* crit, float* acc, int64_t acc_stride,
+                     const int32_t* planted, int n_planted, float bonus, int q_heads, float scale,
+                     cudaStream_t stream, bool* handled) {
+  using namespace umma_attn;
+  *handled = false;
+  const int G = q_heads / kvp->kv_heads;
+  if (kvp->dtype != SD_DTYPE_BF16 || kvp->head_dim != D) return 0;
+  if (!(G == 4 || G == 8)) return 0;
+  const int rows = max_nq * G;
+  const int NR = rows <= 16 ? 16 : rows <= 32 ? 32 : rows <= 48 ? 48 : rows <= 64 ? 64 : 0;
+  if (NR == 0 || NR % G != 0) return 0;
+  static const int wide = env_int("SD_UMMA_WIDE", 0);  // 1: one CTA/SM with 512 TMEM columns
+  const int tcols = wide ? 512 : 256;
+  const int tmax_raw = (tcols - NR) / NR;
+  const int slots = 148 * (wide ? 1 : 2);
+  int C = 1, chunk = TK;
+  if (!plan_umma(max_keys < 1 ? 1 : max_keys, num_items, kvp->kv_heads, tmax_raw, slots, &C, &chunk)) return 0;
+  Params prm;
+  prm.q = static_cast<const __nv_bfloat16*>(q);
+  prm.out = static_cast<__nv_bfloat16*>(out);
+  prm.lse_out = lse;
+  prm.kv = make_paged(kvp);
+  prm.layer = layer;
+  prm.items = items;
+  prm.crit = crit;
+  prm.acc = acc;
+  prm.acc_stride = acc_stride;
+  prm.planted = planted;
+  prm.n_planted = n_planted;
+  prm.bonus_log2 = bonus * LOG2E;
+  prm.q_heads = q_heads;
+  prm.scale_log2 = scale * LOG2E;
+  prm.chunk = chunk;
+  *handled = true;
+#define SD_UMMA_CASE(GG, N)                                                                   \
+  if (G == GG && NR == N) {                                                                   \
+    if (wide) return launch_one<GG, N, 5, 512>(prm, C, num_items, kvp->kv_heads, stream);     \
+    return launch_one<GG, N, 2, 256>(prm, C, num_items, kvp->kv_heads, stream);               \
+  }
+  SD_UMMA_CASE(4, 16) SD_UMMA_CASE(4, 32) SD_UMMA_CASE(4, 48) SD_UMMA_CASE(4, 64)
+  SD_UMMA_CASE(8, 16) SD_UMMA_CASE(8, 32) SD_UMMA_CASE(8, 48) SD_UMMA_CASE(8, 64)
+#undef SD_UMMA_CASE
+  *handled = false;
+  return 0;
+}
+
+}  // namespace sd

@@ -20,7 +20,7 @@ PKG = HERE.parent
 ROOT = PKG.parent
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libspardec_b200.so"
-SOURCES = ["abi.cu", "attn_generic.cu", "attn_mma.cu", "rope_kv.cu", "select.cu", "accept.cu", "glue.cu", "attn_ws.cu", "attn_tm.cu"]
+SOURCES = ["abi.cu", "attn_generic.cu", "attn_mma.cu", "rope_kv.cu", "select.cu", "accept.cu", "glue.cu", "attn_ws.cu", "attn_tm.cu", "attn_umma.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

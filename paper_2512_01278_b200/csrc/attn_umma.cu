@@ -164,31 +164,49 @@ struct Params {
 };
 
 struct Layout {
-  int ring, q, pbuf, pos, bar, wm, wl, rowm, rowl, rowlse, tptr, total;
+  int ring, q, pbuf, pos, slot, bar, wm, wl, rowm, rowl, rowlse, tptr, total;
 };
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
-__host__ __device__ inline Layout make_layout(int NR, int NSLOT, int TMAX) {
+// ct = key tiles of this launch's chunk (positions + physical slots are staged per key)
+__host__ __device__ inline Layout make_layout(int NR, int NSLOT, int TMAX, int ct) {
   Layout L{};
   int o = 0;
   L.ring = o;  o += NSLOT * TILE_BYTES;
   L.q = o;     o += 2 * NR * 128;        // [dhalf][NR][128 B], SWIZZLE_128B
   L.pbuf = o;  o += 2 * NR * TK * 2;     // 2 x P^T [128 keys][NR] bf16, MN-major, no swizzle
-  L.pos = o;   o += TMAX * TK * 4;
+  L.pos = o;   o += ct * TK * 4;
+  L.slot = o;  o += ct * TK * 4;
   o = align_up(o, 8);
-  L.bar = o;   o += (2 * NSLOT + TMAX + 5) * 8;
+  L.bar = o;   o += (2 * NSLOT + 2 * TMAX + 5) * 8;
   L.wm = o;    o += NSW * NR * 4;
   L.wl = o;    o += NSW * NR * 4;
   L.rowm = o;  o += NR * 4;
   L.rowl = o;  o += NR * 4;
   L.rowlse = o; o += NR * 4;
   L.tptr = o;  o += 16;
-  L.total = align_up(o, 1024) + 1024;  // + slack to 1024-align the dynamic base
+  L.total = align_up(o, 128) + 1024;  // + slack to 1024-align the dynamic base
   return L;
+}
+
+// Fill order of the producer ring (each fill = one 32 KB K or V tile):
+//   K[0..nt)                    phase 1 (logits -> TMEM, row statistics)
+//   V[nt-TR..nt)                phase 2 over the TR tiles whose logits are still in TMEM
+//   (K[j], V[j]) j < nt-TR      phase 2 over evicted tiles: K re-read, logits recomputed
+// With nt <= TMAX (TR = nt) every K and V row is read exactly once.
+__device__ __forceinline__ void fill_tile(int f, int nt, int TR, int& t, bool& isv) {
+  if (f < nt) {
+    t = f, isv = false;
+  } else if (f < nt + TR) {
+    t = nt - TR + (f - nt), isv = true;
+  } else {
+    const int g = f - nt - TR;
+    t = g >> 1, isv = g & 1;
+  }
 }
 
 template <int G, int NR, int NSLOT, int TCOLS>
 __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(const Params p) {
-  constexpr int TMAX = (TCOLS - NR) / NR;  // S tiles resident in TMEM
+  constexpr int TMAX = (TCOLS - NR) / NR;  // S tiles resident in TMEM (slot ring)
   constexpr int OCOL = TMAX * NR;          // O^T accumulator columns
   constexpr int NTOK = NR / G;             // token slots covered by NR rows
 
@@ -202,20 +220,24 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
   const int kb = crank * p.chunk;
   const int ke = min(Nk, kb + p.chunk);
   const int nk = max(0, ke - kb);
-  const int ntiles = (nk + TK - 1) / TK;
+  const int nt = (nk + TK - 1) / TK;
+  const int TR = min(nt, TMAX);
+  const int nfill = 3 * nt - TR;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const Layout L = make_layout(NR, NSLOT, TMAX);
+  const Layout L = make_layout(NR, NSLOT, TMAX, p.chunk / TK);
   unsigned char* ring = smem + L.ring;
   unsigned char* qs = smem + L.q;
   unsigned char* pbuf = smem + L.pbuf;
   int32_t* spos = reinterpret_cast<int32_t*>(smem + L.pos);
+  int32_t* sslot = reinterpret_cast<int32_t*>(smem + L.slot);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);
   uint64_t* empty = full + NSLOT;
-  uint64_t* sbar = empty + NSLOT;        // [TMAX] S tile t in TMEM
-  uint64_t* pready = sbar + TMAX;        // [2] P^T buffer written
+  uint64_t* sfull = empty + NSLOT;       // [TMAX] logits of the slot's current use are in TMEM
+  uint64_t* sfree = sfull + TMAX;        // [TMAX] softmax warps are done reading the slot
+  uint64_t* pready = sfree + TMAX;       // [2] P^T buffer written
   uint64_t* pfree = pready + 2;          // [2] P^T buffer consumed by the PV MMA
   uint64_t* obar = pfree + 2;            // O^T complete
   float* wm = reinterpret_cast<float*>(smem + L.wm);
@@ -229,15 +251,34 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
   if (warp == WMMA) tmem_alloc(tptr, TCOLS);
   if (tid == 0) {
     for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, 32), mbar_init(empty + i, 1);
-    for (int i = 0; i < TMAX; ++i) mbar_init(sbar + i, 1);
-    mbar_init(pready + 0, NSW * 32), mbar_init(pready + 1, NSW * 32);
+    for (int i = 0; i < TMAX; ++i) mbar_init(sfull + i, 1), mbar_init(sfree + i, NSW);
+    mbar_init(pready + 0, NSW), mbar_init(pready + 1, NSW);
     mbar_init(pfree + 0, 1), mbar_init(pfree + 1, 1);
     mbar_init(obar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  for (int j = tid; j < ntiles * TK; j += NT) {
-    const int gj = kb + j;
-    spos[j] = gj < ke ? it.key_pos(p.crit, gj) : -1;
+  // key positions and their physical slots for the whole chunk (the producer's
+  // copy loop then never waits on a block-table load); keys past the chunk
+  // copy the last valid row (finite data, masked out of the softmax)
+  {
+    const int nkeys = nt * TK;
+    const int32_t* trow = p.kv.table + (int64_t)it.table_row * p.kv.table_stride;
+    const int pmask = (1 << p.kv.page_shift) - 1;
+    for (int j0 = 0; j0 < nkeys; j0 += 8 * NT) {  // 8 independent loads in flight per thread
+      int pos[8], pg[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pos[k] = it.key_pos(p.crit, min(kb + j0 + k * NT + tid, ke - 1));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pg[k] = __ldg(trow + (pos[k] >> p.kv.page_shift));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = j0 + k * NT + tid;
+        if (j < nkeys) {
+          spos[j] = kb + j < ke ? pos[k] : -1;
+          sslot[j] = (pg[k] << p.kv.page_shift) | (pos[k] & pmask);
+        }
+      }
+    }
   }
   // Q rows (token-major: r = tok*G + g) -> [dhalf][NR][128 B] SWIZZLE_128B, zero padding rows
   for (int i = tid; i < NR * 16; i += NT) {
@@ -260,23 +301,18 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
 
   if (warp == WPROD) {
     // ===================== producer =====================
-    const uint64_t pol = policy_evict_first();  // every row is read exactly once
+    const uint64_t pol = policy_evict_first();  // every row is read once (K of evicted tiles twice)
     const int sub = lane >> 4, c = lane & 15;   // 2 key rows x 16 chunks per instruction
     const uint32_t ring_u = smem_u32(ring);
-    const int last = nk - 1;
-    int sl[4], nsl[4];
-    auto resolve = [&](int t, int (&s)[4]) {
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int j = min(t * TK + m * 32 + lane, last);
-        s[m] = static_cast<int>(p.kv.slot_of(it.table_row, spos[j]));
-      }
-    };
-    if (ntiles > 0) resolve(0, sl);
-    for (int f = 0; f < 2 * ntiles; ++f) {
+    for (int f = 0; f < nfill; ++f) {
       const int s = f % NSLOT;
-      const __nv_bfloat16* base = (f < ntiles ? Kg : Vg) + c * 8;
-      if (f + 1 < 2 * ntiles) resolve(f + 1 < ntiles ? f + 1 : f + 1 - ntiles, nsl);
+      int t;
+      bool isv;
+      fill_tile(f, nt, TR, t, isv);
+      const __nv_bfloat16* base = (isv ? Vg : Kg) + c * 8;
+      int sl[4];  // physical slots of keys lane + 32m, broadcast by shuffles below
+#pragma unroll
+      for (int m = 0; m < 4; ++m) sl[m] = sslot[t * TK + m * 32 + lane];
       if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
       const uint32_t dst0 = ring_u + s * TILE_BYTES + (c >> 3) * (TK * 128);
 #pragma unroll
@@ -286,11 +322,9 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
         cp_async16(dst0 + i * 128 + (((c & 7) ^ (i & 7)) << 4), base + (int64_t)slot * row_stride, pol);
       }
       cp_async_mbar_arrive(full + s);
-#pragma unroll
-      for (int m = 0; m < 4; ++m) sl[m] = nsl[m];
-      if (f == ntiles - 1) cluster_arrive();  // K streamed; let the exchange proceed
+      if (f == nt - 1) cluster_arrive();  // K streamed; let the exchange proceed
     }
-    if (ntiles == 0) cluster_arrive();
+    if (nt == 0) cluster_arrive();
     cluster_wait();
     cluster_arrive();
     cluster_wait();
@@ -305,9 +339,11 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
     const uint32_t id_qk = idesc_bf16(NR, false, false);
     const uint32_t id_pv = idesc_bf16(NR, true, true);
     const bool leader = lane == 0;
-    for (int t = 0; t < ntiles; ++t) {
-      const int s = t % NSLOT;
-      mbar_wait(full + s, (t / NSLOT) & 1);
+    int f = 0;
+    // S^T for use u (tile's logits) into TMEM slot u % TMAX from ring slot s
+    auto qk = [&](int u, int s) {
+      mbar_wait(full + s, (f / NSLOT) & 1);
+      if (u >= TMAX) mbar_wait(sfree + u % TMAX, ((u / TMAX) - 1) & 1);
       fence_proxy_async();
       tc_fence_after();
       if (leader) {
@@ -317,37 +353,40 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
           const uint32_t off = (ks & 3) << 5;  // K = 16 bf16 = 32 B steps inside the 128-B atom
           const uint64_t a = smem_desc(a0 + (ks >> 2) * (TK * 128) + off, 16, 1024, 2);
           const uint64_t b = smem_desc(q_u + (ks >> 2) * (NR * 128) + off, 16, 1024, 2);
-          umma(tbase + t * NR, a, b, id_qk, ks > 0);
+          umma(tbase + (u % TMAX) * NR, a, b, id_qk, ks > 0);
         }
         umma_commit(empty + s);
-        umma_commit(sbar + t);
+        umma_commit(sfull + u % TMAX);
       }
       __syncwarp();
-    }
+      ++f;
+    };
+    for (int t = 0; t < nt; ++t) qk(t, f % NSLOT);
     cluster_arrive();  // barrier 1: this warp's part of phase 1 is issued
-    for (int t = 0; t < ntiles; ++t) {
-      const int f = ntiles + t;
+    for (int i2 = 0; i2 < nt; ++i2) {
+      if (i2 >= TR) qk(nt + (i2 - TR), f % NSLOT);  // evicted tile: recompute its logits
       const int s = f % NSLOT;
       mbar_wait(full + s, (f / NSLOT) & 1);
-      mbar_wait(pready + (t & 1), (t >> 1) & 1);
+      mbar_wait(pready + (i2 & 1), (i2 >> 1) & 1);
       fence_proxy_async();
       tc_fence_after();
       if (leader) {
         const uint32_t a0 = ring_u + s * TILE_BYTES;
-        const uint32_t b0 = p_u + (t & 1) * (NR * TK * 2);
+        const uint32_t b0 = p_u + (i2 & 1) * (NR * TK * 2);
 #pragma unroll
         for (int ks = 0; ks < TK / 16; ++ks) {
           // A = V^T: MN-major SW128, 64-d atoms LBO = 16 KB apart, 8-key groups SBO = 1 KB
           const uint64_t a = smem_desc(a0 + ks * 16 * 128, TK * 128, 1024, 2);
           // B = P^T: MN-major no swizzle, 8-key core groups LBO = 128 B, 8-row groups SBO = 2 KB
           const uint64_t b = smem_desc(b0 + ks * 2 * 128, 128, TK * 16, 0);
-          umma(tbase + OCOL, a, b, id_pv, (t > 0 || ks > 0) ? 1u : 0u);
+          umma(tbase + OCOL, a, b, id_pv, (i2 > 0 || ks > 0) ? 1u : 0u);
         }
         umma_commit(empty + s);
-        umma_commit(pfree + (t & 1));
-        if (t == ntiles - 1) umma_commit(obar);
+        umma_commit(pfree + (i2 & 1));
+        if (i2 == nt - 1) umma_commit(obar);
       }
       __syncwarp();
+      ++f;
     }
     cluster_wait();
     cluster_arrive();
@@ -366,29 +405,34 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
 #pragma unroll
   for (int r = 0; r < NR; ++r) m[r] = -INFINITY, l[r] = 0.f;
 
-  // per-key scalars for tile t: bias and first visible row (rows >= rmin see the key)
+  // per-key scalars for tile t: position, bias and first visible row (rows >= rmin see the key)
   auto key_info = [&](int t, int& pos, float& bias, int& rmin) {
     const int j = t * TK + kl;
     pos = spos[j];
-    const int gj = kb + j;
     if (pos < 0) {
       rmin = NR;  // past the chunk: invisible to every row
       bias = 0.f;
       return;
     }
-    rmin = gj < it.crit_len ? 0 : max(0, pos - it.qpos0) * G;
+    rmin = kb + j < it.crit_len ? 0 : max(0, pos - it.qpos0) * G;
     bias = p.n_planted ? planted_bias(p.planted, p.n_planted, p.bonus_log2, pos) : 0.f;
+  };
+  auto release = [&](int u) {  // one elected arrival per warp
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(sfree + u % TMAX);
   };
 
   // ---- phase 1: S^T tiles -> thread-local online (max, sum) ----
-  for (int t = 0; t < ntiles; ++t) {
+  for (int t = 0; t < nt; ++t) {
     int pos, rmin;
     float bias;
     key_info(t, pos, bias, rmin);
-    mbar_wait(sbar + t, 0);
+    mbar_wait(sfull + t % TMAX, (t / TMAX) & 1);
     tc_fence_after();
     float v[NR];
-    tmem_ld_row<NR>(tl + t * NR, v);
+    tmem_ld_row<NR>(tl + (t % TMAX) * NR, v);
+    if (t < nt - TR) release(t);  // evicted before phase 2: recomputed there
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       if (r >= rmin && r < R) {
@@ -448,12 +492,17 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
 
   // ---- phase 2: P = exp2(S - lse) (final), scores, P^T -> smem for the PV MMA ----
   const bool scores = p.acc != nullptr && it.acc_row >= 0;
-  for (int t = 0; t < ntiles; ++t) {
+  for (int i2 = 0; i2 < nt; ++i2) {
+    const int t = i2 < TR ? nt - TR + i2 : i2 - TR;  // resident tiles first, then the evicted ones
+    const int u = i2 < TR ? t : nt + t;              // TMEM slot use holding its logits
     int pos, rmin;
     float bias;
     key_info(t, pos, bias, rmin);
+    mbar_wait(sfull + u % TMAX, (u / TMAX) & 1);
+    tc_fence_after();
     float v[NR];
-    tmem_ld_row<NR>(tl + t * NR, v);
+    tmem_ld_row<NR>(tl + (u % TMAX) * NR, v);
+    release(u);
 #pragma unroll
     for (int r = 0; r < NR; ++r)
       v[r] = (r >= rmin && r < R) ? ex2(fmaf(v[r], p.scale_log2, bias) - lse[r]) : 0.f;
@@ -474,31 +523,31 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
         }
       }
     }
-    if (t >= 2) mbar_wait(pfree + (t & 1), ((t >> 1) - 1) & 1);
+    if (i2 >= 2) mbar_wait(pfree + (i2 & 1), ((i2 >> 1) - 1) & 1);
     // P^T [key][row]: core matrix (8 keys x 8 rows) = 128 B; key groups 128 B apart,
     // row groups TK*16 B apart -> this thread's 8-row chunks at kl*16 + ng*TK*16
-    unsigned char* pb = pbuf + (t & 1) * (NR * TK * 2) + kl * 16;
+    unsigned char* pb = pbuf + (i2 & 1) * (NR * TK * 2) + kl * 16;
 #pragma unroll
     for (int ng = 0; ng < NR / 8; ++ng) {
       __nv_bfloat162 b0 = __floats2bfloat162_rn(v[ng * 8 + 0], v[ng * 8 + 1]);
       __nv_bfloat162 b1 = __floats2bfloat162_rn(v[ng * 8 + 2], v[ng * 8 + 3]);
       __nv_bfloat162 b2 = __floats2bfloat162_rn(v[ng * 8 + 4], v[ng * 8 + 5]);
       __nv_bfloat162 b3 = __floats2bfloat162_rn(v[ng * 8 + 6], v[ng * 8 + 7]);
-      uint4 u;
-      u.x = *reinterpret_cast<uint32_t*>(&b0);
-      u.y = *reinterpret_cast<uint32_t*>(&b1);
-      u.z = *reinterpret_cast<uint32_t*>(&b2);
-      u.w = *reinterpret_cast<uint32_t*>(&b3);
-      *reinterpret_cast<uint4*>(pb + ng * TK * 16) = u;
+      uint4 w;
+      w.x = *reinterpret_cast<uint32_t*>(&b0);
+      w.y = *reinterpret_cast<uint32_t*>(&b1);
+      w.z = *reinterpret_cast<uint32_t*>(&b2);
+      w.w = *reinterpret_cast<uint32_t*>(&b3);
+      *reinterpret_cast<uint4*>(pb + ng * TK * 16) = w;
     }
     fence_proxy_async();
-    tc_fence_before();
-    mbar_arrive(pready + (t & 1));
+    __syncwarp();
+    if (lane == 0) mbar_arrive(pready + (i2 & 1));
   }
 
   // ---- epilogue: O^T (lane = d) -> cluster reduction -> out ----
   float o[NR];
-  if (ntiles > 0) {
+  if (nt > 0) {
     mbar_wait(obar, 0);
     tc_fence_after();
     tmem_ld_row<NR>(tl + OCOL, o);
@@ -539,12 +588,12 @@ template <int G, int NR, int NSLOT, int TCOLS>
 int launch_one(const Params& prm, int C, int num_items, int kv_heads, cudaStream_t stream) {
   constexpr int TMAX = (TCOLS - NR) / NR;
   auto kern = attn_umma_kernel<G, NR, NSLOT, TCOLS>;
-  const int smem = make_layout(NR, NSLOT, TMAX).total;
-  static bool configured = false;
-  if (!configured) {
+  const int smem = make_layout(NR, NSLOT, TMAX, prm.chunk / TK).total;
+  static int configured = 0;
+  if (smem > configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    configured = true;
+    configured = smem;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C, kv_heads, num_items);
@@ -572,27 +621,38 @@ static int env_int(const char* name, int dflt) {
   return v && *v ? atoi(v) : dflt;
 }
 
+// Key tiles of one CTA's chunk that fit the shared-memory budget (positions + slots staged per key).
+static int chunk_cap_tiles(int NR, int nslot, int tmax, int budget) {
+  int ct = 1;
+  while (ct < 256 && make_layout(NR, nslot, tmax, ct + 1).total <= budget) ++ct;
+  return make_layout(NR, nslot, tmax, ct).total <= budget ? ct : 0;
+}
+
 }  // namespace umma_attn
 
-// Cluster size: smallest C whose chunk fits the TMEM logit store (TMAX tiles),
-// then the C (<= 16) that best fills whole waves of the SM slots.
-static bool plan_umma(int max_keys, int num_items, int kv_heads, int tmax, int slots, int* C_out, int* chunk_out) {
+// Cluster size C (<= 16) and chunk for one launch: minimise (waves of SM slots) x
+// (32 KB fills per CTA + fixed per-CTA cost).  Chunks longer than the TMEM-resident
+// tiles re-read the evicted tiles' K in phase 2 (fills = 3*ct - tmax).
+static bool plan_umma(int max_keys, int num_items, int kv_heads, int tmax, int cap, int slots, int* C_out,
+                      int* chunk_out) {
   using namespace umma_attn;
   const int tiles = (max_keys + TK - 1) / TK;
-  const int c_min = (tiles + tmax - 1) / tmax;
-  if (c_min > 16) return false;
   static const int force_c = env_int("SD_ATTN_C", 0);
-  const int work = num_items * kv_heads;
-  int best = c_min;
-  double best_eff = -1.0;
-  for (int c = c_min; c <= 16 && c <= tiles; ++c) {
-    const int chunk_tiles = (tiles + c - 1) / c;
-    const double waves = (double)work * c / (double)slots;
-    // whole-wave fill x amortisation of the fixed per-CTA cost (~1 tile)
-    const double eff = (waves / (double)((long long)(waves + 0.999999))) * (chunk_tiles / (chunk_tiles + 1.0));
-    if (eff > best_eff + 0.02) best_eff = eff, best = c;
+  static const double ovh = env_int("SD_UMMA_OVH10", 20) / 10.0;
+  const long long work = (long long)num_items * kv_heads;
+  int best = 0;
+  double best_cost = 1e300;
+  for (int c = 1; c <= 16 && c <= tiles; ++c) {
+    const int ct = (tiles + c - 1) / c;
+    if (ct > cap) continue;
+    const double fills = ct <= tmax ? 2.0 * ct : 3.0 * ct - tmax;
+    const long long ctas = work * c;
+    const double waves = (double)((ctas + slots - 1) / slots);
+    const double cost = waves * (fills + ovh);
+    if (cost < best_cost * 0.98) best_cost = cost, best = c;
   }
-  if (force_c >= c_min && force_c <= 16) best = force_c;
+  if (force_c >= 1 && force_c <= 16 && (tiles + force_c - 1) / force_c <= cap) best = force_c;
+  if (best == 0) return false;
   *C_out = best;
   *chunk_out = ((tiles + best - 1) / best) * TK;
   return true;
@@ -610,12 +670,20 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
   const int rows = max_nq * G;
   const int NR = rows <= 16 ? 16 : rows <= 32 ? 32 : rows <= 48 ? 48 : rows <= 64 ? 64 : 0;
   if (NR == 0 || NR % G != 0) return 0;
-  static const int wide = env_int("SD_UMMA_WIDE", 0);  // 1: one CTA/SM with 512 TMEM columns
-  const int tcols = wide ? 512 : 256;
-  const int tmax_raw = (tcols - NR) / NR;
-  const int slots = 148 * (wide ? 1 : 2);
+  static const int wide_env = env_int("SD_UMMA_WIDE", -1);  // 1: one CTA/SM, 512 TMEM columns, 5-slot ring
+  // two CTAs per SM (256 TMEM columns, 2-slot ring each) unless their shared memory does not fit
+  const int narrow_cap = chunk_cap_tiles(NR, 2, (256 - NR) / NR, 113 * 1024);
+  const int wide_cap = chunk_cap_tiles(NR, 5, (512 - NR) / NR, 227 * 1024);
   int C = 1, chunk = TK;
-  if (!plan_umma(max_keys < 1 ? 1 : max_keys, num_items, kvp->kv_heads, tmax_raw, slots, &C, &chunk)) return 0;
+  const int mk = max_keys < 1 ? 1 : max_keys;
+  bool wide = false;
+  if (!(wide_env != 1 && narrow_cap > 0 &&
+        plan_umma(mk, num_items, kvp->kv_heads, (256 - NR) / NR, narrow_cap, 296, &C, &chunk))) {
+    if (wide_env == 0 || wide_cap == 0 ||
+        !plan_umma(mk, num_items, kvp->kv_heads, (512 - NR) / NR, wide_cap, 148, &C, &chunk))
+      return 0;
+    wide = true;
+  }
   Params prm;
   prm.q = static_cast<const __nv_bfloat16*>(q);
   prm.out = static_cast<__nv_bfloat16*>(out);

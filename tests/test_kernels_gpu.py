@@ -167,6 +167,59 @@ def test_batched_items_mixed_lengths_bf16():
             assert np.abs(a[t] - want).max() <= 2e-2
 
 
+@pytest.mark.parametrize("n0,G,nq", [(30000, 4, 5), (12000, 8, 3), (64000, 4, 2)])
+def test_verify_attention_long_context_bf16(n0, G, nq):
+    """Contexts past the TMEM-resident capacity of a 16-CTA cluster: evicted tiles are
+    recomputed in phase 2 (K re-read); outputs, lse and scores must not change."""
+    rng = np.random.default_rng(n0)
+    Hkv, d = 2, 128
+    Hq = Hkv * G
+    pool = _pool(1, Hkv, d, n0 + nq, 1, torch.bfloat16, shuffle_seed=4)
+    _fill(pool, 0, n0 + nq, rng, scale=0.5)
+    kr, vr = pool.read(0, range(n0 + nq))
+    kr, vr = kr.double().cpu().numpy()[:, 0], vr.double().cpu().numpy()[:, 0]
+    q = torch.from_numpy(rng.normal(size=(nq, Hq, d))).to(DEV, torch.bfloat16)
+    out = torch.empty_like(q)
+    lse = torch.empty(nq, Hq, dtype=torch.float32, device=DEV)
+    W = n0 + nq
+    acc = torch.zeros(nq, W, dtype=torch.float32, device=DEV)
+    items = make_items([(0, 0, nq, n0, 0, 0, 0, 0, 1)], DEV)
+    K.attention(q, out, pool, 0, items, 1, n0 + nq, nq, Hq, lse=lse, acc=acc, acc_row_stride=W)
+    torch.cuda.synchronize()
+    ro, rl, ra = _ref_rows(q.double().cpu().numpy(), kr, vr, Hq, Hkv, d, [], range(n0 + nq), n0)
+    assert np.abs(out.double().cpu().numpy() - ro).max() <= 2e-2
+    assert np.abs(lse.double().cpu().numpy() - rl).max() <= 2e-2
+    a = acc.double().cpu().numpy()
+    np.testing.assert_allclose(a.sum(axis=1), Hq * np.ones(nq), rtol=2e-2)
+    for t in range(nq):
+        want = np.zeros(W)
+        for p_, val in ra[t].items():
+            want[p_] = val
+        assert np.abs(a[t] - want).max() <= 2e-2
+
+
+def test_sparse_draft_attention_large_budget_bf16():
+    """10% of a 64K context (6.4K critical keys + fresh tail) in one draft item."""
+    rng = np.random.default_rng(11)
+    Hkv, G, d = 2, 4, 128
+    Hq = Hkv * G
+    n0, j = 64000, 3
+    pool = _pool(1, Hkv, d, n0 + j + 1, 1, torch.bfloat16, shuffle_seed=6)
+    _fill(pool, 0, n0 + j + 1, rng, scale=0.5)
+    kr, vr = pool.read(0, range(n0 + j + 1))
+    kr, vr = kr.double().cpu().numpy()[:, 0], vr.double().cpu().numpy()[:, 0]
+    crit = np.sort(rng.choice(n0, size=6400, replace=False)).astype(np.int32)
+    q = torch.from_numpy(rng.normal(size=(1, Hq, d))).to(DEV, torch.bfloat16)
+    out = torch.empty_like(q)
+    lse = torch.empty(1, Hq, dtype=torch.float32, device=DEV)
+    items = make_items([(0, 0, 1, n0 + j, 0, len(crit), n0, -1, 0)], DEV)
+    K.attention(q, out, pool, 0, items, 1, len(crit) + j + 1, 1, Hq, crit=torch.from_numpy(crit).to(DEV), lse=lse)
+    torch.cuda.synchronize()
+    ro, rl, _ = _ref_rows(q.double().cpu().numpy(), kr, vr, Hq, Hkv, d, crit.tolist(), range(n0, n0 + j + 1), n0 + j)
+    assert np.abs(out.double().cpu().numpy() - ro).max() <= 2e-2
+    assert np.abs(lse.double().cpu().numpy() - rl).max() <= 2e-2
+
+
 def test_topk_golden_kats(golden_topk):
     n = len([k for k in golden_topk if k.endswith(".values")])
     for dt in (torch.float64,):

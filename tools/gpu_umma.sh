@@ -1,7 +1,7 @@
 #!/bin/bash
 # Quick check of the tcgen05 attention kernel: kernel parity tests + microbench.
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_kernels_gpu.py -x -q > gpurun_out/umma_pytest.log 2>&1
+timeout 900 python -m pytest tests/test_kernels_gpu.py -x -q > gpurun_out/umma_pytest.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/umma_pytest.log
-timeout 300 python bench_kernels.py --ctx 4096,8192,32768 --sparsity 0.05 --iters 20 > gpurun_out/umma_kb.log 2>&1
-SD_UMMA_WIDE=1 timeout 300 python bench_kernels.py --ctx 4096,8192,32768 --sparsity 0.05 --iters 20 > gpurun_out/umma_kb_wide.log 2>&1
+timeout 600 python bench_kernels.py --sparsity 0.05 --iters 20 > gpurun_out/umma_kb.log 2>&1
+SD_UMMA_WIDE=1 timeout 600 python bench_kernels.py --sparsity 0.05 --iters 20 > gpurun_out/umma_kb_wide.log 2>&1

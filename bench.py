@@ -432,7 +432,7 @@ def main():
                        "parallelism": f"dp{args.gpus} (request shards, no hot-path collective)",
                        "l2": "inputs larger than L2 (~30 GB read per step)", "pipeline": "synchronous",
                        "alpha": m["alpha"]},
-            "roofline": {"bound": "hbm", "kernel": "K2 verify attention (attn_mma_kernel, score emission)",
+            "roofline": {"bound": "hbm", "kernel": "K2 verify attention (attn_umma_kernel: tcgen05, TMEM-resident logits, score emission)",
                          "achieved": v_gbs, "peak": hbm, "unit": "GB/s", "frac": v_gbs / hbm, "traffic": traffic,
                          "peak_source": peak_src, "launches": m.get("verify_launches"),
                          "draft_kernel": {"achieved": d_gbs, "frac": d_gbs / hbm, "launches": m.get("draft_launches")}},

@@ -98,7 +98,8 @@ int sd_rope_kv_write(const void* qkv, int64_t qkv_row_stride, int32_t rows,
  *              acc[row][pos] += sum over the group's q heads of exp(s - lse)
  *   planted  : device int32 sorted positions receiving +planted_bonus, or NULL
  *   max_keys, max_nq : host upper bounds over items (launch shaping)
- *   workspace: device scratch (see sd_attention_workspace_bytes)
+ *   workspace: ZERO-FILLED device scratch of sd_attention_workspace_bytes() bytes;
+ *              every call leaves it zero-filled again (reuse it across calls)
  *   flags    : bit0 = force the generic (FFMA) kernel */
 int64_t sd_attention_workspace_bytes(int32_t num_items, int32_t max_keys, int32_t max_nq,
                                      int32_t q_heads, const sd_paged_kv* kv);

@@ -23,8 +23,9 @@ int launch_attn_tm(const void* q, void* out, float* lse, const sd_paged_kv* kvp,
                    bool* handled);
 int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer, const int32_t* items,
                      int num_items, int max_keys, int max_nq, const int32_t* crit, float* acc, int64_t acc_stride,
-                     const int32_t* planted, int n_planted, float bonus, int q_heads, float scale,
-                     cudaStream_t stream, bool* handled);
+                     const int32_t* planted, int n_planted, float bonus, int q_heads, float scale, void* ws,
+                     int64_t ws_bytes, cudaStream_t stream, bool* handled);
+int64_t umma_ws_bytes(const sd_paged_kv* kvp, int num_items, int max_keys, int max_nq, int q_heads, bool* handled);
 int launch_attn_ws(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer, const int32_t* items,
                    int num_items, int max_keys, int max_nq, const int32_t* crit, float* acc, int64_t acc_stride,
                    const int32_t* planted, int n_planted, float bonus, int q_heads, float scale, cudaStream_t stream,
@@ -45,6 +46,12 @@ extern "C" int64_t sd_launch_count(void) { return sd::g_launches.load(); }
 extern "C" int64_t sd_attention_workspace_bytes(int32_t num_items, int32_t max_keys, int32_t max_nq,
                                                 int32_t q_heads, const sd_paged_kv* kv) {
   if (kv == nullptr || kv->kv_heads <= 0) return 0;
+  static const char* impl = getenv("SD_ATTN_IMPL");
+  if (!(impl && impl[0] && impl[0] != 'u')) {
+    bool handled = false;
+    const int64_t b = sd::umma_ws_bytes(kv, num_items, max_keys, max_nq, q_heads, &handled);
+    if (handled) return b;
+  }
   const int G = q_heads / kv->kv_heads;
   if (sd::mma_attn_plannable(kv->dtype, kv->head_dim, max_nq * G, max_keys, num_items, kv->kv_heads)) return 0;
   return sd::generic_ws_bytes(num_items, max_keys, max_nq * G, kv->kv_heads);
@@ -73,8 +80,8 @@ extern "C" int sd_attention(const void* q, void* out, float* lse, const sd_paged
   if (!(flags & 1) && use_umma) {
     bool handled = false;
     const int rc = sd::launch_attn_umma(q, out, lse, kv, layer, items, num_items, max_keys, max_nq, crit, acc,
-                                        acc_row_stride, planted, num_planted, planted_bonus, q_heads, scale, s,
-                                        &handled);
+                                        acc_row_stride, planted, num_planted, planted_bonus, q_heads, scale,
+                                        workspace, workspace_bytes, s, &handled);
     if (handled || rc != 0) return rc;
   }
   if (!(flags & 1) && use_tm) {

@@ -163,6 +163,8 @@ int launch_attn_generic(const void* q, void* out, float* lse, const sd_paged_kv*
         max_keys, max_rows);
   }
   count_launch();
+  // workspace contract (spardec_b200.h): handed back zero-filled
+  cudaMemsetAsync(ws, 0, generic_ws_bytes(num_items, max_keys, max_rows, kvp->kv_heads), stream);
   SD_CUDA_RETURN();
 }
 

@@ -145,7 +145,17 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+constexpr int kTraceCtas = 16384;
+constexpr int kTraceSlots = 12;
+__device__ uint64_t g_trace[kTraceCtas * kTraceSlots];
+__device__ __forceinline__ uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct Params {
+  int trace;  // diagnostics: per-CTA phase timestamps (SD_ATTN_TRACE=1)
   const __nv_bfloat16* q;
   __nv_bfloat16* out;
   float* lse_out;
@@ -163,8 +173,38 @@ struct Params {
   int chunk;  // keys per CTA, multiple of TK
 };
 
+// (m, l) softmax-statistics merge
+__device__ __forceinline__ void stat_merge(float& m, float& l, float om, float ol) {
+  const float nm = fmaxf(m, om);
+  l = (nm == -INFINITY) ? 0.f : l * ex2(m - nm) + ol * ex2(om - nm);
+  m = nm;
+}
+// Transpose-reduce N (power of two <= 32) per-row statistics over the warp's 32 keys:
+// halving rounds exchange half of the rows each time (N - 1 shuffles per value instead
+// of 5N), leaving lane L with the full reduction of row L % N in m[0], l[0].
+template <int N>
+__device__ __forceinline__ void warp_rows_reduce(float* m, float* l, int lane) {
+#pragma unroll
+  for (int o = N / 2; o >= 1; o >>= 1) {
+    const bool hi = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float sm = hi ? m[i] : m[i + o], sl = hi ? l[i] : l[i + o];
+      float km = hi ? m[i + o] : m[i], kl = hi ? l[i + o] : l[i];
+      const float rm = __shfl_xor_sync(0xffffffffu, sm, o), rl = __shfl_xor_sync(0xffffffffu, sl, o);
+      stat_merge(km, kl, rm, rl);
+      m[i] = km, l[i] = kl;
+    }
+  }
+#pragma unroll
+  for (int o = N; o < 32; o <<= 1) {
+    const float rm = __shfl_xor_sync(0xffffffffu, m[0], o), rl = __shfl_xor_sync(0xffffffffu, l[0], o);
+    stat_merge(m[0], l[0], rm, rl);
+  }
+}
+
 struct Layout {
-  int ring, q, pbuf, pos, slot, bar, wm, wl, rowm, rowl, rowlse, tptr, total;
+  int ring, q, pbuf, pos, slot, bar, wm, wl, xm, xl, rowlse, tptr, total;
 };
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
 // ct = key tiles of this launch's chunk (positions + physical slots are staged per key)
@@ -180,8 +220,8 @@ __host__ __device__ inline Layout make_layout(int NR, int NSLOT, int TMAX, int c
   L.bar = o;   o += (2 * NSLOT + 2 * TMAX + 5) * 8;
   L.wm = o;    o += NSW * NR * 4;
   L.wl = o;    o += NSW * NR * 4;
-  L.rowm = o;  o += NR * 4;
-  L.rowl = o;  o += NR * 4;
+  L.xm = o;    o += 16 * NR * 4;          // [source CTA][row] pushed by every cluster peer
+  L.xl = o;    o += 16 * NR * 4;
   L.rowlse = o; o += NR * 4;
   L.tptr = o;  o += 16;
   L.total = align_up(o, 128) + 1024;  // + slack to 1024-align the dynamic base
@@ -224,6 +264,17 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
   const int TR = min(nt, TMAX);
   const int nfill = 3 * nt - TR;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#define TRACE(k, val)                                                                                   \
+  do {                                                                                                  \
+    if (p.trace && cta_lin < kTraceCtas) g_trace[cta_lin * kTraceSlots + (k)] = (val);                  \
+  } while (0)
+  if (tid == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    TRACE(0, gtime());
+    TRACE(9, (uint64_t)smid | ((uint64_t)nt << 32));
+  }
 
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -242,8 +293,8 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
   uint64_t* obar = pfree + 2;            // O^T complete
   float* wm = reinterpret_cast<float*>(smem + L.wm);
   float* wl = reinterpret_cast<float*>(smem + L.wl);
-  float* rowm = reinterpret_cast<float*>(smem + L.rowm);
-  float* rowl = reinterpret_cast<float*>(smem + L.rowl);
+  float* xm = reinterpret_cast<float*>(smem + L.xm);
+  float* xl = reinterpret_cast<float*>(smem + L.xl);
   float* rowlse = reinterpret_cast<float*>(smem + L.rowlse);
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L.tptr);
 
@@ -294,6 +345,7 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tptr;
+  if (tid == 0) TRACE(1, gtime());
 
   const int64_t row_stride = (int64_t)p.kv.kv_heads * D;  // elements between consecutive slots
   const __nv_bfloat16* Kg = static_cast<const __nv_bfloat16*>(p.kv.k) + (int64_t)p.layer * p.kv.layer_stride + h * D;
@@ -322,14 +374,20 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
         cp_async16(dst0 + i * 128 + (((c & 7) ^ (i & 7)) << 4), base + (int64_t)slot * row_stride, pol);
       }
       cp_async_mbar_arrive(full + s);
-      if (f == nt - 1) cluster_arrive();  // K streamed; let the exchange proceed
+      if (f == nt - 1) {
+        if (lane == 0) TRACE(11, gtime());
+        if (C > 1) cluster_arrive();  // K streamed; let the exchange proceed
+      }
     }
-    if (nt == 0) cluster_arrive();
-    cluster_wait();
-    cluster_arrive();
-    cluster_wait();
-    cluster_arrive();
-    cluster_wait();
+    if (lane == 0) TRACE(7, gtime());
+    if (C > 1) {
+      if (nt == 0) cluster_arrive();
+      cluster_wait();
+      for (int b = 0; b < 2; ++b) {  // the softmax warps' epilogue barriers
+        cluster_arrive();
+        cluster_wait();
+      }
+    }
     return;
   }
 
@@ -362,7 +420,8 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
       ++f;
     };
     for (int t = 0; t < nt; ++t) qk(t, f % NSLOT);
-    cluster_arrive();  // barrier 1: this warp's part of phase 1 is issued
+    if (lane == 0) TRACE(10, gtime());
+    if (C > 1) cluster_arrive();  // barrier 1: this warp's part of phase 1 is issued
     for (int i2 = 0; i2 < nt; ++i2) {
       if (i2 >= TR) qk(nt + (i2 - TR), f % NSLOT);  // evicted tile: recompute its logits
       const int s = f % NSLOT;
@@ -388,11 +447,14 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
       __syncwarp();
       ++f;
     }
-    cluster_wait();
-    cluster_arrive();
-    cluster_wait();
-    cluster_arrive();
-    cluster_wait();
+    if (C > 1) {
+      cluster_wait();
+      for (int b = 0; b < 2; ++b) {  // the softmax warps' epilogue barriers
+        cluster_arrive();
+        cluster_wait();
+      }
+    }
+    asm volatile("bar.sync 2, %0;\n" ::"n"((NSW + 1) * 32) : "memory");  // softmax warps read O
     tc_fence_after();
     tmem_dealloc(tbase, TCOLS);
     return;
@@ -443,17 +505,19 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
       }
     }
   }
+  if (tid == 0) TRACE(2, gtime());
   // ---- exchange: warp -> CTA -> cluster row statistics -> exact lse ----
 #pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    if (r < R) {
-      float mw = m[r];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
-      float lw = (mw == -INFINITY) ? 0.f : l[r] * ex2(m[r] - mw);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, o);
-      if (lane == 0) wm[warp * NR + r] = mw, wl[warp * NR + r] = lw;
+  for (int b0 = 0; b0 < NR; b0 += 32) {
+    constexpr int NB0 = NR < 32 ? NR : 32;
+    if (NR - b0 >= 32 || NR < 32) {
+      warp_rows_reduce<NB0>(m + b0, l + b0, lane);
+      const int row = b0 + (lane & (NB0 - 1));
+      if (lane < NB0 && row < R) wm[warp * NR + row] = m[b0], wl[warp * NR + row] = l[b0];
+    } else {  // NR = 48: rows 32..47
+      warp_rows_reduce<16>(m + b0, l + b0, lane);
+      const int row = b0 + (lane & 15);
+      if (lane < 16 && row < R) wm[warp * NR + row] = m[b0], wl[warp * NR + row] = l[b0];
     }
   }
   sw_bar();
@@ -466,20 +530,29 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
       ll = (nm == -INFINITY) ? 0.f : ll * ex2(mm - nm) + ol * ex2(om - nm);
       mm = nm;
     }
-    rowm[tid] = mm;
-    rowl[tid] = ll;
+    // push this CTA's row statistics into every peer's [crank][row] slot (remote
+    // stores are fire-and-forget; the cluster barrier's release/acquire orders them)
+    for (int c = 0; c < C; ++c) {
+      *cluster.map_shared_rank(xm + crank * NR + tid, c) = mm;
+      *cluster.map_shared_rank(xl + crank * NR + tid, c) = ll;
+    }
   }
-  cluster_arrive();
-  cluster_wait();
+  if (tid == 0) TRACE(8, gtime());
+  if (C > 1) {
+    cluster_arrive();
+    cluster_wait();
+  } else {
+    sw_bar();
+  }
   if (tid < NR) {
     float lse2 = INFINITY;  // padding rows -> P = 0
     if (tid < R) {
       float M = -INFINITY;
-      for (int c = 0; c < C; ++c) M = fmaxf(M, *cluster.map_shared_rank(rowm + tid, c));
+      for (int c = 0; c < C; ++c) M = fmaxf(M, xm[c * NR + tid]);
       float Ls = 0.f;
       for (int c = 0; c < C; ++c) {
-        const float mc = *cluster.map_shared_rank(rowm + tid, c);
-        if (mc != -INFINITY) Ls += *cluster.map_shared_rank(rowl + tid, c) * ex2(mc - M);
+        const float mc = xm[c * NR + tid];
+        if (mc != -INFINITY) Ls += xl[c * NR + tid] * ex2(mc - M);
       }
       lse2 = M + log2f(Ls);
     }
@@ -489,6 +562,7 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
   float lse[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) lse[r] = rowlse[r];
+  if (tid == 0) TRACE(3, gtime());
 
   // ---- phase 2: P = exp2(S - lse) (final), scores, P^T -> smem for the PV MMA ----
   const bool scores = p.acc != nullptr && it.acc_row >= 0;
@@ -546,6 +620,350 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
   }
 
   // ---- epilogue: O^T (lane = d) -> cluster reduction -> out ----
+  if (tid == 0) TRACE(4, gtime());
+  float o[NR];
+  if (nt > 0) {
+    mbar_wait(obar, 0);
+    tc_fence_after();
+    if (tid == 0) TRACE(5, gtime());
+    tmem_ld_row<NR>(tl + OCOL, o);
+  } else {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) o[r] = 0.f;
+  }
+  tc_fence_before();
+  asm volatile("bar.arrive 2, %0;\n" ::"n"((NSW + 1) * 32) : "memory");  // O read: TMEM may be freed
+  const int dcol = kl;
+  if (C == 1) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+      if (r < R)
+        p.out[((int64_t)(it.q_row0 + r / G) * p.q_heads + h * G + r % G) * D + dcol] = __float2bfloat16_rn(o[r]);
+  } else {
+    // all MMAs of this CTA are complete (obar): its ring holds the O^T partial; row r is
+    // summed over the cluster by CTA r % C (DSMEM loads issued back to back)
+    float* Ob = reinterpret_cast<float*>(ring);  // [NR][D]
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+      if (r < R) Ob[r * D + dcol] = o[r];
+    cluster_arrive();
+    cluster_wait();
+    for (int r = crank; r < R; r += C) {
+      float part[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) part[c] = c < C ? *cluster.map_shared_rank(Ob + r * D + dcol, c) : 0.f;
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) sum += part[c];
+      p.out[((int64_t)(it.q_row0 + r / G) * p.q_heads + h * G + r % G) * D + dcol] = __float2bfloat16_rn(sum);
+    }
+  }
+  if (p.lse_out != nullptr && crank == 0 && tid < R)
+    p.lse_out[(int64_t)(it.q_row0 + tid / G) * p.q_heads + h * G + tid % G] = rowlse[tid] * LN2;
+  if (C > 1) {  // peers may still be reading this CTA's partial
+    cluster_arrive();
+    cluster_wait();
+  }
+  if (tid == 0) TRACE(6, gtime());
+#undef TRACE
+}
+
+// ---------------------------------------------------------------------------------------
+// Head-packed draft kernel (K1, one query token per item): a CTA covers HPC kv heads of one
+// item, and a 128-row UMMA tile is KPT = 128 / HPC keys x HPC heads (head-major rows), so
+//   S^T[(head, key)][HPC*G] = K_rows . Q^T      (only the row's own head block is used)
+//   O^T[d][HPC*G]         += V_rows^T . P^T    (P^T is block-diagonal: exact per head)
+// Every statistic of a (head, q head) row lives inside one warp (KPT = 32 or 16 keys of the
+// tile per head), so there is no CTA exchange; the setup cost is paid once per HPC heads
+// and every fill moves 32 KB however small the critical set is.
+template <int N>
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, float* v) {
+  if constexpr (N == 4) {
+    uint32_t r0, r1, r2, r3;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(taddr) : "memory");
+    v[0] = __uint_as_float(r0), v[1] = __uint_as_float(r1), v[2] = __uint_as_float(r2), v[3] = __uint_as_float(r3);
+  } else if constexpr (N == 8) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr) : "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+  } else {
+    static_assert(N % 16 == 0, "tcgen05.ld width");
+#pragma unroll
+    for (int c = 0; c < N; c += 16) tmem_ld16(taddr + c, v + c);
+  }
+}
+
+template <int G, int HPC, int NSLOT, int TCOLS>
+__global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_hp_kernel(const Params p) {
+  constexpr int NQ = HPC * G;                       // q heads of the CTA
+  constexpr int NR = NQ < 16 ? 16 : NQ;             // UMMA N
+  constexpr int KPT = TK / HPC;                     // keys per tile
+  constexpr int TMAX = (TCOLS - NR) / NR;
+  constexpr int OCOL = TMAX * NR;
+  constexpr int WH = KPT >= 32 ? 1 : 32 / KPT;      // heads per warp (rows of a warp)
+  static_assert(KPT == 16 || KPT == 32, "head packing: 4 or 8 heads per CTA");
+
+  const int h0 = blockIdx.x * HPC;
+  const Item it = load_item(p.items, blockIdx.y);
+  const int nk = it.num_keys();
+  const int nt = (nk + KPT - 1) / KPT;
+  const int TR = min(nt, TMAX);
+  const int nfill = 3 * nt - TR;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const Layout L = make_layout(NR, NSLOT, TMAX, (nt * KPT + TK - 1) / TK);
+  unsigned char* ring = smem + L.ring;
+  unsigned char* qs = smem + L.q;
+  unsigned char* pbuf = smem + L.pbuf;
+  int32_t* spos = reinterpret_cast<int32_t*>(smem + L.pos);
+  int32_t* sslot = reinterpret_cast<int32_t*>(smem + L.slot);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);
+  uint64_t* empty = full + NSLOT;
+  uint64_t* sfull = empty + NSLOT;
+  uint64_t* sfree = sfull + TMAX;
+  uint64_t* pready = sfree + TMAX;
+  uint64_t* pfree = pready + 2;
+  uint64_t* obar = pfree + 2;
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L.tptr);
+
+  if (warp == WMMA) tmem_alloc(tptr, TCOLS);
+  if (tid == 0) {
+    for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, 32), mbar_init(empty + i, 1);
+    for (int i = 0; i < TMAX; ++i) mbar_init(sfull + i, 1), mbar_init(sfree + i, NSW);
+    mbar_init(pready + 0, NSW), mbar_init(pready + 1, NSW);
+    mbar_init(pfree + 0, 1), mbar_init(pfree + 1, 1);
+    mbar_init(obar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  {
+    const int nkeys = nt * KPT;
+    const int32_t* trow = p.kv.table + (int64_t)it.table_row * p.kv.table_stride;
+    const int pmask = (1 << p.kv.page_shift) - 1;
+    for (int j0 = 0; j0 < nkeys; j0 += 8 * NT) {
+      int pos[8], pg[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pos[k] = it.key_pos(p.crit, min(j0 + k * NT + tid, nk - 1));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pg[k] = __ldg(trow + (pos[k] >> p.kv.page_shift));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = j0 + k * NT + tid;
+        if (j < nkeys) {
+          spos[j] = j < nk ? pos[k] : -1;
+          sslot[j] = (pg[k] << p.kv.page_shift) | (pos[k] & pmask);
+        }
+      }
+    }
+  }
+  // Q: the CTA's NQ q heads are contiguous in the row (heads h0.. x group)
+  for (int i = tid; i < NR * 16; i += NT) {
+    const int r = i >> 4, c = i & 15;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < NQ) v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)it.q_row0 * p.q_heads + h0 * G + r) * D + c * 8);
+    *reinterpret_cast<uint4*>(qs + (c >> 3) * (NR * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+  }
+  // P^T buffers: off-diagonal blocks stay zero for the whole launch
+  for (int i = tid; i < 2 * NR * TK * 2 / 16; i += NT) reinterpret_cast<uint4*>(pbuf)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tptr;
+
+  const int64_t row_stride = (int64_t)p.kv.kv_heads * D;
+  const __nv_bfloat16* Kg = static_cast<const __nv_bfloat16*>(p.kv.k) + (int64_t)p.layer * p.kv.layer_stride + h0 * D;
+  const __nv_bfloat16* Vg = static_cast<const __nv_bfloat16*>(p.kv.v) + (int64_t)p.layer * p.kv.layer_stride + h0 * D;
+
+  if (warp == WPROD) {
+    const uint64_t pol = policy_evict_first();
+    const int sub = lane >> 4, c = lane & 15;
+    const uint32_t ring_u = smem_u32(ring);
+    for (int f = 0; f < nfill; ++f) {
+      const int s = f % NSLOT;
+      int t;
+      bool isv;
+      fill_tile(f, nt, TR, t, isv);
+      const __nv_bfloat16* base = (isv ? Vg : Kg) + c * 8;
+      const int sl = sslot[t * KPT + (lane % KPT)];
+      if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
+      const uint32_t dst0 = ring_u + s * TILE_BYTES + (c >> 3) * (TK * 128);
+#pragma unroll
+      for (int kk = 0; kk < TK / 2; ++kk) {
+        const int i = 2 * kk + sub;            // tile row = head-major (hh, key)
+        const int hh = (2 * kk) / KPT;         // same for both rows of the instruction
+        const int slot = __shfl_sync(0xffffffffu, sl, ((2 * kk) % KPT) + sub);
+        cp_async16(dst0 + i * 128 + (((c & 7) ^ (i & 7)) << 4), base + (int64_t)slot * row_stride + hh * D, pol);
+      }
+      cp_async_mbar_arrive(full + s);
+    }
+    return;
+  }
+
+  if (warp == WMMA) {
+    const uint32_t ring_u = smem_u32(ring), q_u = smem_u32(qs), p_u = smem_u32(pbuf);
+    const uint32_t id_qk = idesc_bf16(NR, false, false);
+    const uint32_t id_pv = idesc_bf16(NR, true, true);
+    const bool leader = lane == 0;
+    int f = 0;
+    auto qk = [&](int u, int s) {
+      mbar_wait(full + s, (f / NSLOT) & 1);
+      if (u >= TMAX) mbar_wait(sfree + u % TMAX, ((u / TMAX) - 1) & 1);
+      fence_proxy_async();
+      tc_fence_after();
+      if (leader) {
+        const uint32_t a0 = ring_u + s * TILE_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t off = (ks & 3) << 5;
+          const uint64_t a = smem_desc(a0 + (ks >> 2) * (TK * 128) + off, 16, 1024, 2);
+          const uint64_t b = smem_desc(q_u + (ks >> 2) * (NR * 128) + off, 16, 1024, 2);
+          umma(tbase + (u % TMAX) * NR, a, b, id_qk, ks > 0);
+        }
+        umma_commit(empty + s);
+        umma_commit(sfull + u % TMAX);
+      }
+      __syncwarp();
+      ++f;
+    };
+    for (int t = 0; t < nt; ++t) qk(t, f % NSLOT);
+    for (int i2 = 0; i2 < nt; ++i2) {
+      if (i2 >= TR) qk(nt + (i2 - TR), f % NSLOT);
+      const int s = f % NSLOT;
+      mbar_wait(full + s, (f / NSLOT) & 1);
+      mbar_wait(pready + (i2 & 1), (i2 >> 1) & 1);
+      fence_proxy_async();
+      tc_fence_after();
+      if (leader) {
+        const uint32_t a0 = ring_u + s * TILE_BYTES;
+        const uint32_t b0 = p_u + (i2 & 1) * (NR * TK * 2);
+#pragma unroll
+        for (int ks = 0; ks < TK / 16; ++ks) {
+          const uint64_t a = smem_desc(a0 + ks * 16 * 128, TK * 128, 1024, 2);
+          const uint64_t b = smem_desc(b0 + ks * 2 * 128, 128, TK * 16, 0);
+          umma(tbase + OCOL, a, b, id_pv, (i2 > 0 || ks > 0) ? 1u : 0u);
+        }
+        umma_commit(empty + s);
+        umma_commit(pfree + (i2 & 1));
+        if (i2 == nt - 1) umma_commit(obar);
+      }
+      __syncwarp();
+      ++f;
+    }
+    asm volatile("bar.sync 2, %0;\n" ::"n"((NSW + 1) * 32) : "memory");
+    tc_fence_after();
+    tmem_dealloc(tbase, TCOLS);
+    return;
+  }
+
+  // ===================== softmax warps: thread = (head, key) row of the tile =====================
+  const int row = warp * 32 + lane;
+  const int hh = row / KPT, k = row % KPT;
+  const int hsel = WH > 1 ? (lane / KPT) : 0;            // which of the warp's heads
+  const int col0 = (warp * 32 / KPT) * G;                // first S column the warp reads
+  const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
+  float m[G], l[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) m[g] = -INFINITY, l[g] = 0.f;
+
+  auto load_s = [&](int u, float (&v)[G]) {
+    float w[WH * G];
+    tmem_ld_n<WH * G>(tl + (u % TMAX) * NR + col0, w);
+    tmem_wait_ld();
+#pragma unroll
+    for (int g = 0; g < G; ++g) v[g] = WH > 1 && hsel ? w[G + g] : w[g];
+  };
+  auto key_info = [&](int t, int& pos, float& bias, bool& vis) {
+    const int j = t * KPT + k;
+    pos = spos[j];
+    vis = pos >= 0 && (j < it.crit_len || pos <= it.qpos0);
+    bias = (vis && p.n_planted) ? planted_bias(p.planted, p.n_planted, p.bonus_log2, pos) : 0.f;
+  };
+  auto release = [&](int u) {
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(sfree + u % TMAX);
+  };
+
+  for (int t = 0; t < nt; ++t) {
+    int pos;
+    float bias;
+    bool vis;
+    key_info(t, pos, bias, vis);
+    mbar_wait(sfull + t % TMAX, (t / TMAX) & 1);
+    tc_fence_after();
+    float v[G];
+    load_s(t, v);
+    if (t < nt - TR) release(t);
+    if (vis) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float s2 = fmaf(v[g], p.scale_log2, bias);
+        const float nm = fmaxf(m[g], s2);
+        l[g] = l[g] * ex2(m[g] - nm) + ex2(s2 - nm);
+        m[g] = nm;
+      }
+    }
+  }
+  // statistics of each (head, q head) row: reduce over the KPT lanes of this head
+  float lse[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+#pragma unroll
+    for (int o = KPT / 2; o >= 1; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, m[g], o), ol = __shfl_xor_sync(0xffffffffu, l[g], o);
+      stat_merge(m[g], l[g], om, ol);
+    }
+    lse[g] = m[g] + log2f(l[g]);
+  }
+
+  const bool scores = p.acc != nullptr && it.acc_row >= 0;
+  for (int i2 = 0; i2 < nt; ++i2) {
+    const int t = i2 < TR ? nt - TR + i2 : i2 - TR;
+    const int u = i2 < TR ? t : nt + t;
+    int pos;
+    float bias;
+    bool vis;
+    key_info(t, pos, bias, vis);
+    mbar_wait(sfull + u % TMAX, (u / TMAX) & 1);
+    tc_fence_after();
+    float v[G];
+    load_s(u, v);
+    release(u);
+    float sum = 0.f;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      v[g] = vis ? ex2(fmaf(v[g], p.scale_log2, bias) - lse[g]) : 0.f;
+      sum += v[g];
+    }
+    if (scores && sum != 0.f) red_add(p.acc + (int64_t)it.acc_row * p.acc_stride + pos, sum);
+    if (i2 >= 2) mbar_wait(pfree + (i2 & 1), ((i2 >> 1) - 1) & 1);
+    // P^T row `row`: this head's G columns (the rest of the row stays zero)
+    unsigned char* pb = pbuf + (i2 & 1) * (NR * TK * 2) + row * 16 + ((hh * G) >> 3) * (TK * 16);
+    if constexpr (G == 8) {
+      uint4 w;
+      __nv_bfloat162 b0 = __floats2bfloat162_rn(v[0], v[1]), b1 = __floats2bfloat162_rn(v[2], v[3]);
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(v[4], v[5]), b3 = __floats2bfloat162_rn(v[6], v[7]);
+      w.x = *reinterpret_cast<uint32_t*>(&b0), w.y = *reinterpret_cast<uint32_t*>(&b1);
+      w.z = *reinterpret_cast<uint32_t*>(&b2), w.w = *reinterpret_cast<uint32_t*>(&b3);
+      *reinterpret_cast<uint4*>(pb) = w;
+    } else {
+      static_assert(G == 4, "group size 4 or 8");
+      uint2 w;
+      __nv_bfloat162 b0 = __floats2bfloat162_rn(v[0], v[1]), b1 = __floats2bfloat162_rn(v[2], v[3]);
+      w.x = *reinterpret_cast<uint32_t*>(&b0), w.y = *reinterpret_cast<uint32_t*>(&b1);
+      *reinterpret_cast<uint2*>(pb + ((hh * G) & 7) * 2) = w;
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(pready + (i2 & 1));
+  }
+
   float o[NR];
   if (nt > 0) {
     mbar_wait(obar, 0);
@@ -555,33 +973,35 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
 #pragma unroll
     for (int r = 0; r < NR; ++r) o[r] = 0.f;
   }
-  const int dcol = kl;
-  if (C == 1) {
-#pragma unroll
-    for (int r = 0; r < NR; ++r)
-      if (r < R)
-        p.out[((int64_t)(it.q_row0 + r / G) * p.q_heads + h * G + r % G) * D + dcol] = __float2bfloat16_rn(o[r]);
-    cluster_arrive();
-    cluster_wait();
-  } else {
-    // all MMAs of this CTA are complete (obar): the ring is free for the O^T partial
-    float* Ob = reinterpret_cast<float*>(ring);  // [NR][D]
-#pragma unroll
-    for (int r = 0; r < NR; ++r)
-      if (r < R) Ob[r * D + dcol] = o[r];
-    cluster_arrive();
-    cluster_wait();
-    for (int r = crank; r < R; r += C) {
-      float sum = 0.f;
-      for (int c = 0; c < C; ++c) sum += *cluster.map_shared_rank(Ob + r * D + dcol, c);
-      p.out[((int64_t)(it.q_row0 + r / G) * p.q_heads + h * G + r % G) * D + dcol] = __float2bfloat16_rn(sum);
-    }
-  }
-  if (p.lse_out != nullptr && crank == 0 && tid < R)
-    p.lse_out[(int64_t)(it.q_row0 + tid / G) * p.q_heads + h * G + tid % G] = rowlse[tid] * LN2;
   tc_fence_before();
-  cluster_arrive();
-  cluster_wait();
+  asm volatile("bar.arrive 2, %0;\n" ::"n"((NSW + 1) * 32) : "memory");
+#pragma unroll
+  for (int r = 0; r < NQ; ++r)
+    p.out[((int64_t)it.q_row0 * p.q_heads + h0 * G + r) * D + row] = __float2bfloat16_rn(o[r]);
+  if (p.lse_out != nullptr && k == 0) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) p.lse_out[(int64_t)it.q_row0 * p.q_heads + (h0 + hh) * G + g] = lse[g] * LN2;
+  }
+}
+
+template <int G, int HPC, int NSLOT, int TCOLS>
+int launch_hp(const Params& prm, int num_items, int kv_heads, int ct, cudaStream_t stream) {
+  constexpr int NQ = HPC * G, NR = NQ < 16 ? 16 : NQ, TMAX = (TCOLS - NR) / NR;
+  auto kern = attn_umma_hp_kernel<G, HPC, NSLOT, TCOLS>;
+  const int smem = make_layout(NR, NSLOT, TMAX, ct).total;
+  static int configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = smem;
+  }
+  kern<<<dim3(kv_heads / HPC, num_items), NT, smem, stream>>>(prm);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("sd_attention (umma, head-packed) launch: ") + cudaGetErrorString(e));
+    return (int)e;
+  }
+  return 0;
 }
 
 template <int G, int NR, int NSLOT, int TCOLS>
@@ -658,33 +1078,89 @@ static bool plan_umma(int max_keys, int num_items, int kv_heads, int tmax, int c
   return true;
 }
 
-int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer, const int32_t* items,
-                     int num_items, int max_keys, int max_nq, const int32_t* crit, float* acc, int64_t acc_stride,
-                     const int32_t* planted, int n_planted, float bonus, int q_heads, float scale,
-                     cudaStream_t stream, bool* handled) {
+struct UmmaPlan {
+  int NR, C, chunk;
+  bool wide;
+};
+
+static bool umma_plan(const sd_paged_kv* kvp, int num_items, int max_keys, int max_nq, int q_heads, UmmaPlan* pl) {
   using namespace umma_attn;
-  *handled = false;
   const int G = q_heads / kvp->kv_heads;
-  if (kvp->dtype != SD_DTYPE_BF16 || kvp->head_dim != D) return 0;
-  if (!(G == 4 || G == 8)) return 0;
+  if (kvp->dtype != SD_DTYPE_BF16 || kvp->head_dim != D) return false;
+  if (!(G == 4 || G == 8)) return false;
   const int rows = max_nq * G;
   const int NR = rows <= 16 ? 16 : rows <= 32 ? 32 : rows <= 48 ? 48 : rows <= 64 ? 64 : 0;
-  if (NR == 0 || NR % G != 0) return 0;
+  if (NR == 0 || NR % G != 0) return false;
   static const int wide_env = env_int("SD_UMMA_WIDE", -1);  // 1: one CTA/SM, 512 TMEM columns, 5-slot ring
   // two CTAs per SM (256 TMEM columns, 2-slot ring each) unless their shared memory does not fit
   const int narrow_cap = chunk_cap_tiles(NR, 2, (256 - NR) / NR, 113 * 1024);
   const int wide_cap = chunk_cap_tiles(NR, 5, (512 - NR) / NR, 227 * 1024);
-  int C = 1, chunk = TK;
   const int mk = max_keys < 1 ? 1 : max_keys;
+  int C = 1, chunk = TK;
   bool wide = false;
   if (!(wide_env != 1 && narrow_cap > 0 &&
         plan_umma(mk, num_items, kvp->kv_heads, (256 - NR) / NR, narrow_cap, 296, &C, &chunk))) {
     if (wide_env == 0 || wide_cap == 0 ||
         !plan_umma(mk, num_items, kvp->kv_heads, (512 - NR) / NR, wide_cap, 148, &C, &chunk))
-      return 0;
+      return false;
     wide = true;
   }
+  pl->NR = NR, pl->C = C, pl->chunk = chunk, pl->wide = wide;
+  return true;
+}
+
+int64_t umma_ws_bytes(const sd_paged_kv* kvp, int num_items, int max_keys, int max_nq, int q_heads, bool* handled) {
+  UmmaPlan pl;
+  *handled = umma_plan(kvp, num_items, max_keys, max_nq, q_heads, &pl);
+  return 0;  // O partials meet in DSMEM: no workspace
+}
+
+int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer, const int32_t* items,
+                     int num_items, int max_keys, int max_nq, const int32_t* crit, float* acc, int64_t acc_stride,
+                     const int32_t* planted, int n_planted, float bonus, int q_heads, float scale, void* ws,
+                     int64_t ws_bytes, cudaStream_t stream, bool* handled) {
+  using namespace umma_attn;
+  *handled = false;
+  static const int hp_env = env_int("SD_UMMA_HP", 1);
+  {
+    const int G = q_heads / kvp->kv_heads;
+    if (hp_env && max_nq == 1 && kvp->dtype == SD_DTYPE_BF16 && kvp->head_dim == D && (G == 4 || G == 8) &&
+        kvp->kv_heads % 4 == 0) {
+      // 4 heads per CTA, 32 keys per tile, the whole key list in one CTA
+      const int NR = 4 * G, tmax = (256 - NR) / NR;
+      const int ct_tiles = (max(max_keys, 1) + 31) / 32;      // 32-key tiles
+      const int ct = (ct_tiles * 32 + TK - 1) / TK;           // 128-key units for the staging arrays
+      if (ct_tiles <= tmax && make_layout(NR, 2, tmax, ct).total <= 113 * 1024) {  // logits stay resident
+        Params prm{};
+        prm.q = static_cast<const __nv_bfloat16*>(q);
+        prm.out = static_cast<__nv_bfloat16*>(out);
+        prm.lse_out = lse;
+        prm.kv = make_paged(kvp);
+        prm.layer = layer;
+        prm.items = items;
+        prm.crit = crit;
+        prm.acc = acc;
+        prm.acc_stride = acc_stride;
+        prm.planted = planted;
+        prm.n_planted = n_planted;
+        prm.bonus_log2 = bonus * LOG2E;
+        prm.q_heads = q_heads;
+        prm.scale_log2 = scale * LOG2E;
+        prm.chunk = ct * TK;
+        *handled = true;
+        if (G == 4) return launch_hp<4, 4, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
+        return launch_hp<8, 4, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
+      }
+    }
+  }
+  UmmaPlan pl;
+  if (!umma_plan(kvp, num_items, max_keys, max_nq, q_heads, &pl)) return 0;
+  const int G = q_heads / kvp->kv_heads;
+  const int NR = pl.NR, C = pl.C;
+  const bool wide = pl.wide;
   Params prm;
+  (void)ws;
+  (void)ws_bytes;
   prm.q = static_cast<const __nv_bfloat16*>(q);
   prm.out = static_cast<__nv_bfloat16*>(out);
   prm.lse_out = lse;
@@ -699,7 +1175,9 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
   prm.bonus_log2 = bonus * LOG2E;
   prm.q_heads = q_heads;
   prm.scale_log2 = scale * LOG2E;
-  prm.chunk = chunk;
+  prm.chunk = pl.chunk;
+  static const int trace = env_int("SD_ATTN_TRACE", 0);
+  prm.trace = trace;
   *handled = true;
 #define SD_UMMA_CASE(GG, N)                                                                   \
   if (G == GG && NR == N) {                                                                   \
@@ -714,3 +1192,13 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
 }
 
 }  // namespace sd
+
+// Diagnostics: per-CTA phase timestamps of the last traced umma launch (SD_ATTN_TRACE=1):
+// [ctas][10] uint64 = start, setup done, phase 1 done, lse known, phase 2 done, O ready,
+// end, producer done, -, smid | tiles << 32.
+extern "C" int sd_attention_trace_umma(uint64_t* host_dst, int32_t ctas) {
+  if (ctas > sd::umma_attn::kTraceCtas) ctas = sd::umma_attn::kTraceCtas;
+  cudaError_t e = cudaMemcpyFromSymbol(host_dst, sd::umma_attn::g_trace,
+                                       sizeof(uint64_t) * sd::umma_attn::kTraceSlots * ctas);
+  return e == cudaSuccess ? 0 : (int)e;
+}

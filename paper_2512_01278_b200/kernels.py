@@ -27,6 +27,20 @@ def rope_kv_write(qkv: torch.Tensor, row_table: torch.Tensor, row_pos: torch.Ten
                                      q_out.data_ptr(), N.stream_handle()), "sd_rope_kv_write")
 
 
+_WS: dict = {}
+
+
+def _zeroed_workspace(nbytes: int, device) -> torch.Tensor:
+    """Per-device attention workspace: zero-filled when allocated, and every
+    sd_attention call hands it back zero-filled (spardec_b200.h), so it is reused."""
+    key = torch.device(device)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=key)
+        _WS[key] = ws
+    return ws
+
+
 def attention(q: torch.Tensor, out: torch.Tensor, pool, layer: int, items: torch.Tensor, num_items: int,
               max_keys: int, max_nq: int, q_heads: int, *, crit: torch.Tensor | None = None,
               lse: torch.Tensor | None = None, acc: torch.Tensor | None = None, acc_row_stride: int = 0,
@@ -42,7 +56,7 @@ def attention(q: torch.Tensor, out: torch.Tensor, pool, layer: int, items: torch
         G = q_heads // pool.kv_heads
         need = num_items * pool.kv_heads * (max_nq * G * max_keys + 3 * max_keys) * 4
     if need > 0 and (workspace is None or workspace.numel() * workspace.element_size() < need):
-        workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+        workspace = _zeroed_workspace(need, q.device)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     if scale is None:
         scale = 1.0 / (pool.head_dim ** 0.5)

@@ -131,6 +131,41 @@ def test_sparse_draft_attention_matches_oracle(dtype, force_generic, d):
     assert np.abs(lse.double().cpu().numpy() - rl).max() <= tol
 
 
+@pytest.mark.parametrize("G,use_planted", [(4, True), (8, False), (8, True)])
+def test_draft_attention_head_packed_bf16(G, use_planted):
+    """Draft items of several requests (4 kv heads per CTA, block-diagonal P): outputs and
+    lse per request vs the oracle over critical U fresh U self, with the planted bias."""
+    rng = np.random.default_rng(20 + G)
+    Hkv, d, B = 8, 128, 3
+    Hq = Hkv * G
+    n0 = 2000
+    pool = _pool(1, Hkv, d, n0 + 4, B, torch.bfloat16, shuffle_seed=7)
+    for r in range(B):
+        _fill(pool, r, n0 + 4, rng)
+    buds = [37, 130, 200]
+    js = [0, 1, 3]
+    crit = [np.sort(rng.choice(n0, size=b, replace=False)).astype(np.int32) for b in buds]
+    planted = np.array(sorted(set(int(x) for x in crit[1][:3]) | {n0 + 1}), dtype=np.int32)
+    offs = np.cumsum([0] + buds)
+    crit_dev = torch.from_numpy(np.concatenate(crit)).to(DEV)
+    q = torch.from_numpy(rng.normal(size=(B, Hq, d))).to(DEV, torch.bfloat16)
+    out = torch.empty_like(q)
+    lse = torch.empty(B, Hq, dtype=torch.float32, device=DEV)
+    items = make_items([(r, r, 1, n0 + js[r], int(offs[r]), buds[r], n0, -1, 0) for r in range(B)], DEV)
+    K.attention(q, out, pool, 0, items, B, max(b + j + 1 for b, j in zip(buds, js)), 1, Hq, crit=crit_dev, lse=lse,
+                planted=torch.from_numpy(planted).to(DEV) if use_planted else None,
+                planted_bonus=2.5 if use_planted else 0.0)
+    torch.cuda.synchronize()
+    for r in range(B):
+        kr, vr = pool.read(r, range(n0 + 4))
+        kr, vr = kr.double().cpu().numpy()[:, 0], vr.double().cpu().numpy()[:, 0]
+        ro, rl, _ = _ref_rows(q[r:r + 1].double().cpu().numpy(), kr, vr, Hq, Hkv, d, crit[r].tolist(),
+                              range(n0, n0 + js[r] + 1), n0 + js[r],
+                              planted=tuple(planted.tolist()) if use_planted else (), bonus=2.5)
+        assert np.abs(out[r:r + 1].double().cpu().numpy() - ro).max() <= 2e-2
+        assert np.abs(lse[r:r + 1].double().cpu().numpy() - rl).max() <= 2e-2
+
+
 def test_batched_items_mixed_lengths_bf16():
     """Many items of ragged length in one launch (cluster split > 1)."""
     rng = np.random.default_rng(5)

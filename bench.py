@@ -178,9 +178,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         bytes_acc = {"verify": 0.0, "draft": 0.0}
         stream = torch.cuda.current_stream()
 
-        def timer(kind, start):
+        def timer(kind, start):  # on the stream the launch is issued on (draft: side stream)
             e = torch.cuda.Event(enable_timing=True)
-            e.record(stream)
+            e.record(torch.cuda.current_stream())
             if start:
                 ev[kind].append([e, None])
             else:

@@ -220,6 +220,19 @@ class AttnLaunch:
     timer: object | None = None   # optional callable(start: bool) for per-launch timing
 
 
+CONCURRENT_LAUNCHES = True  # overlap the attention launches of one layer on two streams
+_SIDE: dict = {}
+
+
+def _side_stream(device) -> torch.cuda.Stream:
+    key = torch.device(device)
+    st = _SIDE.get(key)
+    if st is None:
+        st = torch.cuda.Stream(device=key)
+        _SIDE[key] = st
+    return st
+
+
 def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_table: torch.Tensor,
                  row_pos: torch.Tensor, launches: Sequence[AttnLaunch], lse_out: torch.Tensor | None = None,
                  force_generic: bool = False) -> torch.Tensor:
@@ -241,19 +254,40 @@ def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_t
     hn = torch.empty(R, c.hidden_dim, dtype=dt, device=model.device)
     q_buf = torch.empty(R, Hq, d, dtype=dt, device=model.device)
     ctx = torch.empty(R, Hq, d, dtype=dt, device=model.device)
+    main = torch.cuda.current_stream(model.device)
+    side = (_side_stream(model.device) if len(launches) > 1 and CONCURRENT_LAUNCHES and not force_generic
+            and model.dtype == torch.bfloat16 else None)
+    ev_in = torch.cuda.Event() if side is not None else None
+    ev_out = torch.cuda.Event() if side is not None else None
+
+    def attend(ln, l):
+        if ln.timer is not None:
+            ln.timer(True)
+        K.attention(q_buf, ctx, pool, l, ln.items, ln.num_items, ln.max_keys, ln.max_nq, Hq,
+                    crit=ln.crit, lse=None if lse_out is None else lse_out[l], acc=ln.acc,
+                    acc_row_stride=ln.acc_row_stride, planted=model.planted_dev,
+                    planted_bonus=model.planted_bonus, force_generic=force_generic)
+        if ln.timer is not None:
+            ln.timer(False)
+
     for l in range(c.num_layers):
         K.rmsnorm_cast(x, hn, RMS_EPS)
         qkv = torch.mm(hn, model.w_qkv[l])
         K.rope_kv_write(qkv, row_table, row_pos, pool, l, Hq, q_buf)
-        for ln in launches:
-            if ln.timer is not None:
-                ln.timer(True)
-            K.attention(q_buf, ctx, pool, l, ln.items, ln.num_items, ln.max_keys, ln.max_nq, Hq,
-                        crit=ln.crit, lse=None if lse_out is None else lse_out[l], acc=ln.acc,
-                        acc_row_stride=ln.acc_row_stride, planted=model.planted_dev,
-                        planted_bonus=model.planted_bonus, force_generic=force_generic)
-            if ln.timer is not None:
-                ln.timer(False)
+        if side is None:
+            for ln in launches:
+                attend(ln, l)
+        else:
+            # the launches touch disjoint rows of q / ctx (and disjoint score rows): the later
+            # ones (draft items) run on a side stream and fill the tail waves of the first
+            ev_in.record(main)
+            side.wait_event(ev_in)
+            with torch.cuda.stream(side):
+                for ln in launches[1:]:
+                    attend(ln, l)
+            ev_out.record(side)
+            attend(launches[0], l)
+            main.wait_event(ev_out)
         x = _residual_add(x, ctx.view(R, Hq * d), model.wo[l])
         K.rmsnorm_cast(x, hn, RMS_EPS)
         hm = torch.mm(hn, model.mlp_in[l])

@@ -239,14 +239,14 @@ class BatchedDecoder:
         if R == 0:
             return StepResult({}, 0, 0, 0, 0)
         launches = []
-        if d_items:
-            launches.append(AttnLaunch(_items(d_items, self.dev), len(d_items), d_max_keys, 1, crit=self.crit,
-                                       timer=self._timer("draft")))
         if v_items:
             slots = torch.tensor([s.slot for s in verifs], device=self.dev)
             self.acc.view(self.max_requests, self.k + 1, self.acc_w)[slots] = 0.0
             launches.append(AttnLaunch(_items(v_items, self.dev), len(v_items), v_max_keys, v_max_nq, acc=self.acc,
                                        acc_row_stride=self.acc_w, timer=self._timer("verify")))
+        if d_items:  # after the verify launch: it runs on the side stream (model.forward_rows)
+            launches.append(AttnLaunch(_items(d_items, self.dev), len(d_items), d_max_keys, 1, crit=self.crit,
+                                       timer=self._timer("draft")))
         tok_dev = _i32(toks, self.dev)
         x = forward_rows(self.model, self.pool, tok_dev, _i32(rt, self.dev), _i32(rp, self.dev), launches)
         targets = _argmax(lm_head(self.model, x))

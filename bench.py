@@ -408,8 +408,12 @@ def main():
         d_gbs = m["draft_bytes"] / (m["draft_ms_total"] / 1000.0) / 1e9 if m.get("draft_ms_total") else 0.0
         traffic = None
         tf = ROOT / "profiles" / "k2_traffic.json"
-        if tf.exists():
-            traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+        if tf.exists() and m.get("verify_launches"):
+            # ncu dram bytes / algorithmic bytes of the committed K2 capture, applied to this
+            # run's average algorithmic bytes per K2 launch
+            ratio = json.loads(tf.read_text()).get("traffic_over_algorithmic")
+            if ratio:
+                traffic = ratio * m["verify_bytes"] / m["verify_launches"]
         cpu = None
         if not args.no_cpu_baseline:
             r = cpu_round_sample(args, layers_used=args.cpu_sample_layers)
@@ -434,6 +438,7 @@ def main():
                        "alpha": m["alpha"]},
             "roofline": {"bound": "hbm", "kernel": "K2 verify attention (attn_umma_kernel: tcgen05, TMEM-resident logits, score emission)",
                          "achieved": v_gbs, "peak": hbm, "unit": "GB/s", "frac": v_gbs / hbm, "traffic": traffic,
+                         "traffic_source": "profiles/k2_traffic.json (ncu dram/algorithmic ratio x this run's bytes per launch)",
                          "peak_source": peak_src, "launches": m.get("verify_launches"),
                          "draft_kernel": {"achieved": d_gbs, "frac": d_gbs / hbm, "launches": m.get("draft_launches")}},
             "cpu_baseline": cpu,

@@ -72,10 +72,6 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
-// bulk L2 prefetch of one contiguous row (no shared memory involved)
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
@@ -159,8 +155,7 @@ __device__ __forceinline__ uint64_t gtime() {
 }
 
 struct Params {
-  int trace;     // diagnostics: per-CTA phase timestamps (SD_ATTN_TRACE=1)
-  int prefetch;  // L2 prefetch distance in ring fills (SD_UMMA_PF)
+  int trace;  // diagnostics: per-CTA phase timestamps (SD_ATTN_TRACE=1)
   const __nv_bfloat16* q;
   __nv_bfloat16* out;
   float* lse_out;
@@ -361,19 +356,6 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
     const uint64_t pol = policy_evict_first();  // every row is read once (K of evicted tiles twice)
     const int sub = lane >> 4, c = lane & 15;   // 2 key rows x 16 chunks per instruction
     const uint32_t ring_u = smem_u32(ring);
-    // L2 prefetch runs PF fills ahead of the ring: rows are pulled from HBM while the ring is
-    // still full (e.g. during the cluster exchange), so the later 16-byte copies hit in L2
-    const int PF = p.prefetch;
-    auto prefetch_fill = [&](int f) {
-      if (f >= nfill) return;
-      int t;
-      bool isv;
-      fill_tile(f, nt, TR, t, isv);
-      const __nv_bfloat16* base = isv ? Vg : Kg;
-#pragma unroll
-      for (int m = 0; m < 4; ++m) prefetch_l2(base + (int64_t)sslot[t * TK + m * 32 + lane] * row_stride, D * 2);
-    };
-    for (int f = 0; f < PF; ++f) prefetch_fill(f);
     for (int f = 0; f < nfill; ++f) {
       const int s = f % NSLOT;
       int t;
@@ -383,7 +365,6 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
       int sl[4];  // physical slots of keys lane + 32m, broadcast by shuffles below
 #pragma unroll
       for (int m = 0; m < 4; ++m) sl[m] = sslot[t * TK + m * 32 + lane];
-      if (PF > 0) prefetch_fill(f + PF);
       if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
       const uint32_t dst0 = ring_u + s * TILE_BYTES + (c >> 3) * (TK * 128);
 #pragma unroll
@@ -1197,8 +1178,6 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
   prm.chunk = pl.chunk;
   static const int trace = env_int("SD_ATTN_TRACE", 0);
   prm.trace = trace;
-  static const int pf = env_int("SD_UMMA_PF", 0);
-  prm.prefetch = pf;
   *handled = true;
 #define SD_UMMA_CASE(GG, N)                                                                   \
   if (G == GG && NR == N) {                                                                   \

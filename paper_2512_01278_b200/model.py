@@ -220,7 +220,9 @@ class AttnLaunch:
     timer: object | None = None   # optional callable(start: bool) for per-launch timing
 
 
-CONCURRENT_LAUNCHES = True  # overlap the attention launches of one layer on two streams
+# Overlapping the verify and draft launches of a layer on two streams was measured SLOWER
+# (1810 vs 1947 tokens/s on configs[1]: the two kernels starve each other's CTAs), so off.
+CONCURRENT_LAUNCHES = False
 _SIDE: dict = {}
 
 

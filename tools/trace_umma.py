@@ -89,3 +89,13 @@ for s in np.unique(smid):
     cov2 += (a >= 2).mean()
 ns = len(np.unique(smid))
 print(f"  SM-time with >=1 CTA streaming {cov1 / ns:.2f}, with 2 {cov2 / ns:.2f}")
+# max CTAs alive at once on one SM (start..end overlap)
+mx = 0
+for s_ in np.unique(smid):
+    m = smid == s_
+    ev = sorted([(a, 1) for a in st[m, 0]] + [(b, -1) for b in st[m, 6]], key=lambda x: (x[0], x[1]))
+    cur = 0
+    for _, dlt in ev:
+        cur += dlt
+        mx = max(mx, cur)
+print(f"  max CTAs alive on one SM: {mx}")

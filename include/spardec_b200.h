@@ -146,6 +146,39 @@ int sd_greedy_accept(const int32_t* targets, const int32_t* tokens, const int32_
 int sd_rmsnorm_cast(const float* x, int32_t rows, int32_t h, float eps, void* out, int32_t out_dtype,
                     void* stream);
 
+/* One layer's bf16 weights, row-major [in][out] (model.py:77-105). */
+typedef struct sd_layer_weights {
+  const void* w_qkv;   /* [h][(q_heads + 2 kv_heads) d] = [wq | wk | wv] */
+  const void* wo;      /* [h][h]   */
+  const void* mlp_in;  /* [h][2h]  */
+  const void* mlp_out; /* [2h][h]  */
+} sd_layer_weights;
+
+/* One sd_attention launch per layer (arguments as in sd_attention). */
+typedef struct sd_attn_launch {
+  const int32_t* items;
+  int32_t num_items;
+  int32_t max_keys;
+  int32_t max_nq;
+  int32_t reserved;
+  const int32_t* crit;
+  float* acc;
+  int64_t acc_row_stride;
+} sd_attn_launch;
+
+/* The whole layer stack of one batched forward (model.py:290-342 for `rows` rows at
+ * once; bf16 pools): per layer rmsnorm -> QKV GEMM -> K5 -> sd_attention for each launch
+ * -> out-projection GEMM into the fp32 residual x -> rmsnorm -> MLP-in GEMM -> tanh ->
+ * MLP-out GEMM into x.  GEMMs are cuBLAS (bf16 in, fp32 accumulate).  Buffers:
+ * x fp32 [rows][h] (in/out); hn bf16 [rows][h]; qkv bf16 [rows][(q_heads+2kv_heads)d];
+ * q, ctx bf16 [rows][q_heads][d]; hm bf16 [rows][2h]. */
+int sd_forward_layers(const sd_layer_weights* weights, int32_t layers, float* x, void* hn, void* qkv, void* q,
+                      void* ctx, void* hm, int32_t rows, int32_t hidden, int32_t q_heads,
+                      const int32_t* row_table, const int32_t* row_pos, const sd_paged_kv* kv,
+                      const sd_attn_launch* launches, int32_t num_launches, const int32_t* planted,
+                      int32_t num_planted, float planted_bonus, float scale, float eps, void* workspace,
+                      int64_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

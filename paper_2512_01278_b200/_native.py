@@ -36,6 +36,17 @@ class PagedKvDesc(ctypes.Structure):
 
 
 # name -> (restype, argtypes); must match include/spardec_b200.h
+class LayerWeights(ctypes.Structure):
+    _fields_ = [("w_qkv", ctypes.c_void_p), ("wo", ctypes.c_void_p), ("mlp_in", ctypes.c_void_p),
+                ("mlp_out", ctypes.c_void_p)]
+
+
+class AttnLaunchDesc(ctypes.Structure):
+    _fields_ = [("items", ctypes.c_void_p), ("num_items", ctypes.c_int32), ("max_keys", ctypes.c_int32),
+                ("max_nq", ctypes.c_int32), ("reserved", ctypes.c_int32), ("crit", ctypes.c_void_p),
+                ("acc", ctypes.c_void_p), ("acc_row_stride", ctypes.c_int64)]
+
+
 SIGNATURES = {
     "sd_abi_version": (_i32, []),
     "sd_last_error": (ctypes.c_char_p, []),
@@ -52,6 +63,10 @@ SIGNATURES = {
     "sd_argmax_rows": (ctypes.c_int, [_c_p, _i32, _i64, _i32, _i32, _c_p, _c_p]),
     "sd_greedy_accept": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i32, _c_p, _c_p, _c_p]),
     "sd_rmsnorm_cast": (ctypes.c_int, [_c_p, _i32, _i32, ctypes.c_float, _c_p, _i32, _c_p]),
+    "sd_forward_layers": (ctypes.c_int, [ctypes.POINTER(LayerWeights), _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                         _i32, _i32, _i32, _c_p, _c_p, ctypes.POINTER(PagedKvDesc),
+                                         ctypes.POINTER(AttnLaunchDesc), _i32, _c_p, _i32, ctypes.c_float,
+                                         ctypes.c_float, ctypes.c_float, _c_p, _i64, _c_p]),
 }
 
 _LIB = None

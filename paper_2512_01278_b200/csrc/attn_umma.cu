@@ -845,14 +845,14 @@ static int chunk_cap_tiles(int NR, int nslot, int tmax, int budget) {
 }  // namespace umma_attn
 
 // Cluster size C (<= 16) and chunk for one launch: minimise (waves of SM slots) x
-// (32 KB fills per CTA + fixed per-CTA cost).  Chunks longer than the TMEM-resident
+// (32 KB fills per CTA + fixed per-CTA cost ~7 fills, fitted to traced C sweeps).  Chunks longer than the TMEM-resident
 // tiles re-read the evicted tiles' K in phase 2 (fills = 3*ct - tmax).
 static bool plan_umma(int max_keys, int num_items, int kv_heads, int tmax, int cap, int slots, int* C_out,
                       int* chunk_out) {
   using namespace umma_attn;
   const int tiles = (max_keys + TK - 1) / TK;
   static const int force_c = env_int("SD_ATTN_C", 0);
-  static const double ovh = env_int("SD_UMMA_OVH10", 20) / 10.0;
+  static const double ovh = env_int("SD_UMMA_OVH10", 70) / 10.0;
   const long long work = (long long)num_items * kv_heads;
   int best = 0;
   double best_cost = 1e300;

@@ -20,7 +20,7 @@ PKG = HERE.parent
 ROOT = PKG.parent
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libspardec_b200.so"
-SOURCES = ["abi.cu", "attn_generic.cu", "attn_mma.cu", "rope_kv.cu", "select.cu", "accept.cu", "glue.cu", "attn_ws.cu", "attn_tm.cu", "attn_umma.cu"]
+SOURCES = ["abi.cu", "attn_generic.cu", "attn_mma.cu", "rope_kv.cu", "select.cu", "accept.cu", "glue.cu", "attn_ws.cu", "attn_tm.cu", "attn_umma.cu", "forward.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(tmp), *map(str, objs),
-           "-lcudart"]
+           "-lcudart", "-lcublas"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")

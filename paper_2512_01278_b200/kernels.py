@@ -28,6 +28,7 @@ def rope_kv_write(qkv: torch.Tensor, row_table: torch.Tensor, row_pos: torch.Ten
 
 
 _WS: dict = {}
+_NEED: list = [None, 0]  # last (descriptor, launch shape) -> workspace bytes
 
 
 def _zeroed_workspace(nbytes: int, device) -> torch.Tensor:
@@ -51,7 +52,12 @@ def attention(q: torch.Tensor, out: torch.Tensor, pool, layer: int, items: torch
         return
     desc = pool.desc()
     lib = N.lib()
-    need = lib.sd_attention_workspace_bytes(num_items, max_keys, max_nq, q_heads, ctypes.byref(desc))
+    key = (desc.kv_heads, desc.head_dim, desc.dtype, num_items, max_keys, max_nq, q_heads)
+    if key == _NEED[0]:  # every layer of one iteration asks the same question
+        need = _NEED[1]
+    else:
+        need = lib.sd_attention_workspace_bytes(num_items, max_keys, max_nq, q_heads, ctypes.byref(desc))
+        _NEED[0], _NEED[1] = key, need
     if force_generic:
         G = q_heads // pool.kv_heads
         need = num_items * pool.kv_heads * (max_nq * G * max_keys + 3 * max_keys) * 4

@@ -17,6 +17,8 @@ kernels; there is no CPU path.
 
 from __future__ import annotations
 
+import ctypes
+
 import math
 from dataclasses import dataclass
 from typing import Sequence
@@ -253,6 +255,9 @@ def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_t
     Hq, d = c.num_q_heads, c.head_dim
     dt = model.dtype
     x = model.embedding.index_select(0, tokens.long()).float()
+    if (NATIVE_FORWARD and dt == torch.bfloat16 and lse_out is None and not force_generic
+            and all(ln.timer is None for ln in launches)):
+        return _forward_native(model, pool, tokens, row_table, row_pos, launches, x)
     hn = torch.empty(R, c.hidden_dim, dtype=dt, device=model.device)
     q_buf = torch.empty(R, Hq, d, dtype=dt, device=model.device)
     ctx = torch.empty(R, Hq, d, dtype=dt, device=model.device)
@@ -295,6 +300,55 @@ def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_t
         hm = torch.mm(hn, model.mlp_in[l])
         torch.tanh_(hm)
         x = _residual_add(x, hm, model.mlp_out[l])
+    return x
+
+
+NATIVE_FORWARD = True  # bf16: the layer loop runs in the library (sd_forward_layers), one host call
+
+
+def _forward_native(model: ToyModel, pool: PagedKvPool, tokens, row_table, row_pos, launches, x):
+    """forward_rows for bf16 pools through sd_forward_layers: the same per-layer launches
+    (glue, cuBLAS GEMMs, K5, K1/K2) issued from C++ instead of Python."""
+    c = model.config
+    R = tokens.shape[0]
+    Hq, d, h = c.num_q_heads, c.head_dim, c.hidden_dim
+    dev, dt = model.device, model.dtype
+    lib = N.lib()
+    wts = getattr(model, "_native_weights", None)
+    if wts is None:
+        wts = (N.LayerWeights * c.num_layers)()
+        for l in range(c.num_layers):
+            wts[l].w_qkv = model.w_qkv[l].data_ptr()
+            wts[l].wo = model.wo[l].data_ptr()
+            wts[l].mlp_in = model.mlp_in[l].data_ptr()
+            wts[l].mlp_out = model.mlp_out[l].data_ptr()
+        model._native_weights = wts
+    desc = pool.desc()
+    descs = (N.AttnLaunchDesc * max(1, len(launches)))()
+    need = 0
+    for i, ln in enumerate(launches):
+        descs[i].items = ln.items.data_ptr()
+        descs[i].num_items = ln.num_items
+        descs[i].max_keys = ln.max_keys
+        descs[i].max_nq = ln.max_nq
+        descs[i].crit = N.ptr(ln.crit)
+        descs[i].acc = N.ptr(ln.acc)
+        descs[i].acc_row_stride = ln.acc_row_stride
+        need = max(need, lib.sd_attention_workspace_bytes(ln.num_items, ln.max_keys, ln.max_nq, Hq,
+                                                          ctypes.byref(desc)))
+    ws = K._zeroed_workspace(need, dev) if need > 0 else None
+    qkv_w = (Hq + 2 * c.num_kv_heads) * d
+    hn = torch.empty(R, h, dtype=dt, device=dev)
+    qkv = torch.empty(R, qkv_w, dtype=dt, device=dev)
+    q = torch.empty(R, Hq, d, dtype=dt, device=dev)
+    ctx = torch.empty(R, Hq, d, dtype=dt, device=dev)
+    hm = torch.empty(R, 2 * h, dtype=dt, device=dev)
+    n_planted = 0 if model.planted_dev is None else model.planted_dev.numel()
+    N.check(lib.sd_forward_layers(wts, c.num_layers, x.data_ptr(), hn.data_ptr(), qkv.data_ptr(), q.data_ptr(),
+                                  ctx.data_ptr(), hm.data_ptr(), R, h, Hq, row_table.data_ptr(), row_pos.data_ptr(),
+                                  ctypes.byref(desc), descs, len(launches), N.ptr(model.planted_dev), n_planted,
+                                  model.planted_bonus, 1.0 / math.sqrt(d), RMS_EPS, N.ptr(ws),
+                                  0 if ws is None else ws.numel(), N.stream_handle()), "sd_forward_layers")
     return x
 
 

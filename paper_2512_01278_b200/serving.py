@@ -91,6 +91,7 @@ class BatchedDecoder:
         self.free_slots = list(range(max_requests - 1, -1, -1))
         self.seqs: dict = {}
         self.attn_timer = None       # optional callable(kind, start) for per-launch timing
+        self.host_times: list = []   # per step: (host enqueue s, enqueue + device drain s)
         self.last_rows = 0
 
     # -- lifecycle ------------------------------------------------------------------
@@ -201,6 +202,7 @@ class BatchedDecoder:
         """Run every draft member one draft step and every verify member its
         verification, as one batched forward (engine.py:196-260 semantics)."""
         c = self.model.config
+        t_host0 = time.perf_counter()
         toks, rt, rp = [], [], []
         d_items, v_items = [], []
         drafts = [self.seqs[r] for r in draft_ids]
@@ -250,6 +252,7 @@ class BatchedDecoder:
         tok_dev = _i32(toks, self.dev)
         x = forward_rows(self.model, self.pool, tok_dev, _i32(rt, self.dev), _i32(rp, self.dev), launches)
         targets = _argmax(lm_head(self.model, x))
+        t_launched = time.perf_counter()
         if verifs:
             row0_d, n_d = _i32(v_row0, self.dev), _i32(v_n, self.dev)
             acc_d = torch.empty(len(verifs), dtype=torch.int32, device=self.dev)
@@ -258,6 +261,8 @@ class BatchedDecoder:
             host = torch.cat([targets, acc_d, bonus_d]).cpu().numpy()
         else:
             host = targets.cpu().numpy()
+        t_synced = time.perf_counter()
+        self.host_times.append((t_launched - t_host0, t_synced - t_host0))
         tg = host[:R]
         emitted = 0
         for i, s in enumerate(drafts):

@@ -490,6 +490,23 @@ __device__ __forceinline__ void tmem_ld_n(uint32_t taddr, float* v) {
   }
 }
 
+// shared-memory layout of the head-packed kernel: no cross-warp statistics arrays
+__host__ __device__ inline Layout make_hp_layout(int NR, int NSLOT, int TMAX, int ct) {
+  Layout L{};
+  int o = 0;
+  L.ring = o;  o += NSLOT * TILE_BYTES;
+  L.q = o;     o += 2 * NR * 128;
+  L.pbuf = o;  o += 2 * NR * TK * 2;
+  L.pos = o;   o += ct * TK * 4;
+  L.slot = o;  o += ct * TK * 4;
+  o = align_up(o, 8);
+  L.bar = o;   o += (2 * NSLOT + 2 * TMAX + 5) * 8;
+  L.tptr = o;  o += 16;
+  L.wm = L.wl = L.xm = L.xl = L.rowlse = 0;
+  L.total = align_up(o, 128) + 1024;
+  return L;
+}
+
 template <int G, int HPC, int NSLOT, int TCOLS>
 __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_hp_kernel(const Params p) {
   constexpr int NQ = HPC * G;                       // q heads of the CTA
@@ -510,7 +527,7 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_hp_kernel(
 
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const Layout L = make_layout(NR, NSLOT, TMAX, (nt * KPT + TK - 1) / TK);
+  const Layout L = make_hp_layout(NR, NSLOT, TMAX, (nt * KPT + TK - 1) / TK);
   unsigned char* ring = smem + L.ring;
   unsigned char* qs = smem + L.q;
   unsigned char* pbuf = smem + L.pbuf;
@@ -781,7 +798,7 @@ template <int G, int HPC, int NSLOT, int TCOLS>
 int launch_hp(const Params& prm, int num_items, int kv_heads, int ct, cudaStream_t stream) {
   constexpr int NQ = HPC * G, NR = NQ < 16 ? 16 : NQ, TMAX = (TCOLS - NR) / NR;
   auto kern = attn_umma_hp_kernel<G, HPC, NSLOT, TCOLS>;
-  const int smem = make_layout(NR, NSLOT, TMAX, ct).total;
+  const int smem = make_hp_layout(NR, NSLOT, TMAX, ct).total;
   static int configured = 0;
   if (smem > configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -924,7 +941,7 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
       const int NR = 4 * G, tmax = (256 - NR) / NR;
       const int ct_tiles = (max(max_keys, 1) + 31) / 32;      // 32-key tiles
       const int ct = (ct_tiles * 32 + TK - 1) / TK;           // 128-key units for the staging arrays
-      if (ct_tiles <= tmax && make_layout(NR, 2, tmax, ct).total <= 113 * 1024) {  // logits stay resident
+      if (ct_tiles <= tmax && make_hp_layout(NR, 2, tmax, ct).total <= 113 * 1024) {  // logits stay resident
         Params prm{};
         prm.q = static_cast<const __nv_bfloat16*>(q);
         prm.out = static_cast<__nv_bfloat16*>(out);
@@ -942,8 +959,14 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
         prm.scale_log2 = scale * LOG2E;
         prm.chunk = ct * TK;
         *handled = true;
-        if (G == 4) return launch_hp<4, 4, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
-        return launch_hp<8, 4, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
+        // a third 32 KB ring slot when two CTAs per SM still fit (deeper loads in flight)
+        static const int hp_slots = env_int("SD_UMMA_HP_SLOTS", 3);
+        const bool three = hp_slots == 3 && make_hp_layout(NR, 3, tmax, ct).total <= 113 * 1024;
+        if (G == 4)
+          return three ? launch_hp<4, 4, 3, 256>(prm, num_items, kvp->kv_heads, ct, stream)
+                       : launch_hp<4, 4, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
+        return three ? launch_hp<8, 4, 3, 256>(prm, num_items, kvp->kv_heads, ct, stream)
+                     : launch_hp<8, 4, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
       }
     }
   }

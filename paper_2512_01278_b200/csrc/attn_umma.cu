@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
 
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const Layout L = make_layout(NR, NSLOT, TMAX, p.chunk / TK);
+  const Layout L = make_layout(NR, NSLOT, TMAX, p.chunk / TK, p.dense);
   unsigned char* ring = smem + L.ring;
   unsigned char* qs = smem + L.q;
   unsigned char* pbuf = smem + L.pbuf;
@@ -101,29 +101,48 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
     mbar_init(obar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  // key positions and their physical slots for the whole chunk (the producer's
-  // copy loop then never waits on a block-table load); keys past the chunk
-  // copy the last valid row (finite data, masked out of the softmax)
-  {
+  // key positions and their physical slots for the whole chunk (the producer's copy loop
+  // then never waits on a block-table load); keys past the chunk copy the last valid row
+  // (finite data, masked out of the softmax).  Dense items stage only the page ids.
+  const int32_t* trow = p.kv.table + (int64_t)it.table_row * p.kv.table_stride;
+  const int pshift = p.kv.page_shift, pmask = (1 << pshift) - 1;
+  const int dpos0 = it.dense_lo + kb;          // dense: position of chunk key 0
+  const int dpage0 = dpos0 >> pshift;
+  int32_t* spage = spos;                       // dense: [page - dpage0] -> physical page
+  if (p.dense) {
+    if (nk > 0) {
+      const int lastpg = (it.dense_lo + ke - 1) >> pshift;
+      const int npg = ((dpos0 + nt * TK - 1) >> pshift) - dpage0 + 1;
+      for (int i = tid; i < npg; i += NT) spage[i] = __ldg(trow + min(dpage0 + i, lastpg));
+    }
+  } else {
     const int nkeys = nt * TK;
-    const int32_t* trow = p.kv.table + (int64_t)it.table_row * p.kv.table_stride;
-    const int pmask = (1 << p.kv.page_shift) - 1;
     for (int j0 = 0; j0 < nkeys; j0 += 8 * NT) {  // 8 independent loads in flight per thread
       int pos[8], pg[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) pos[k] = it.key_pos(p.crit, min(kb + j0 + k * NT + tid, ke - 1));
 #pragma unroll
-      for (int k = 0; k < 8; ++k) pg[k] = __ldg(trow + (pos[k] >> p.kv.page_shift));
+      for (int k = 0; k < 8; ++k) pg[k] = __ldg(trow + (pos[k] >> pshift));
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int j = j0 + k * NT + tid;
         if (j < nkeys) {
           spos[j] = kb + j < ke ? pos[k] : -1;
-          sslot[j] = (pg[k] << p.kv.page_shift) | (pos[k] & pmask);
+          sslot[j] = (pg[k] << pshift) | (pos[k] & pmask);
         }
       }
     }
   }
+  // chunk-relative key j -> absolute position (-1 past the chunk) / physical slot
+  auto pos_of = [&](int j) -> int {
+    if (p.dense) return kb + j < ke ? dpos0 + j : -1;
+    return spos[j];
+  };
+  auto slot_of = [&](int j) -> int {
+    if (!p.dense) return sslot[j];
+    const int pos = it.dense_lo + min(kb + j, ke - 1);
+    return (spage[(pos >> pshift) - dpage0] << pshift) | (pos & pmask);
+  };
   // Q rows (token-major: r = tok*G + g) -> [dhalf][NR][128 B] SWIZZLE_128B, zero padding rows
   for (int i = tid; i < NR * 16; i += NT) {
     const int r = i >> 4, c = i & 15;
@@ -157,7 +176,7 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
       const __nv_bfloat16* base = (isv ? Vg : Kg) + c * 8;
       int sl[4];  // physical slots of keys lane + 32m, broadcast by shuffles below
 #pragma unroll
-      for (int m = 0; m < 4; ++m) sl[m] = sslot[t * TK + m * 32 + lane];
+      for (int m = 0; m < 4; ++m) sl[m] = slot_of(t * TK + m * 32 + lane);
       if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
       const uint32_t dst0 = ring_u + s * TILE_BYTES + (c >> 3) * (TK * 128);
 #pragma unroll
@@ -263,7 +282,7 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
   // per-key scalars for tile t: position, bias and first visible row (rows >= rmin see the key)
   auto key_info = [&](int t, int& pos, float& bias, int& rmin) {
     const int j = t * TK + kl;
-    pos = spos[j];
+    pos = pos_of(j);
     if (pos < 0) {
       rmin = NR;  // past the chunk: invisible to every row
       bias = 0.f;
@@ -818,7 +837,7 @@ template <int G, int NR, int NSLOT, int TCOLS>
 int launch_one(const Params& prm, int C, int num_items, int kv_heads, cudaStream_t stream) {
   constexpr int TMAX = (TCOLS - NR) / NR;
   auto kern = attn_umma_kernel<G, NR, NSLOT, TCOLS>;
-  const int smem = make_layout(NR, NSLOT, TMAX, prm.chunk / TK).total;
+  const int smem = make_layout(NR, NSLOT, TMAX, prm.chunk / TK, prm.dense).total;
   static int configured = 0;
   if (smem > configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -853,10 +872,10 @@ static int env_int(const char* name, int dflt) {
 }
 
 // Key tiles of one CTA's chunk that fit the shared-memory budget (positions + slots staged per key).
-static int chunk_cap_tiles(int NR, int nslot, int tmax, int budget) {
+static int chunk_cap_tiles(int NR, int nslot, int tmax, int budget, int dense) {
   int ct = 1;
-  while (ct < 256 && make_layout(NR, nslot, tmax, ct + 1).total <= budget) ++ct;
-  return make_layout(NR, nslot, tmax, ct).total <= budget ? ct : 0;
+  while (ct < 512 && make_layout(NR, nslot, tmax, ct + 1, dense).total <= budget) ++ct;
+  return make_layout(NR, nslot, tmax, ct, dense).total <= budget ? ct : 0;
 }
 
 }  // namespace umma_attn
@@ -894,7 +913,8 @@ struct UmmaPlan {
   bool wide;
 };
 
-static bool umma_plan(const sd_paged_kv* kvp, int num_items, int max_keys, int max_nq, int q_heads, UmmaPlan* pl) {
+static bool umma_plan(const sd_paged_kv* kvp, int num_items, int max_keys, int max_nq, int q_heads, int dense,
+                      UmmaPlan* pl) {
   using namespace umma_attn;
   const int G = q_heads / kvp->kv_heads;
   if (kvp->dtype != SD_DTYPE_BF16 || kvp->head_dim != D) return false;
@@ -904,8 +924,8 @@ static bool umma_plan(const sd_paged_kv* kvp, int num_items, int max_keys, int m
   if (NR == 0 || NR % G != 0) return false;
   static const int wide_env = env_int("SD_UMMA_WIDE", -1);  // 1: one CTA/SM, 512 TMEM columns, 5-slot ring
   // two CTAs per SM (256 TMEM columns, 2-slot ring each) unless their shared memory does not fit
-  const int narrow_cap = chunk_cap_tiles(NR, 2, (256 - NR) / NR, 113 * 1024);
-  const int wide_cap = chunk_cap_tiles(NR, 5, (512 - NR) / NR, 227 * 1024);
+  const int narrow_cap = chunk_cap_tiles(NR, 2, (256 - NR) / NR, 113 * 1024, dense);
+  const int wide_cap = chunk_cap_tiles(NR, 5, (512 - NR) / NR, 227 * 1024, dense);
   const int mk = max_keys < 1 ? 1 : max_keys;
   int C = 1, chunk = TK;
   bool wide = false;
@@ -922,7 +942,7 @@ static bool umma_plan(const sd_paged_kv* kvp, int num_items, int max_keys, int m
 
 int64_t umma_ws_bytes(const sd_paged_kv* kvp, int num_items, int max_keys, int max_nq, int q_heads, bool* handled) {
   UmmaPlan pl;
-  *handled = umma_plan(kvp, num_items, max_keys, max_nq, q_heads, &pl);
+  *handled = umma_plan(kvp, num_items, max_keys, max_nq, q_heads, 1, &pl);
   return 0;  // O partials meet in DSMEM: no workspace
 }
 
@@ -971,7 +991,8 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
     }
   }
   UmmaPlan pl;
-  if (!umma_plan(kvp, num_items, max_keys, max_nq, q_heads, &pl)) return 0;
+  const int dense = (crit == nullptr && kvp->page_shift >= 4) ? 1 : 0;
+  if (!umma_plan(kvp, num_items, max_keys, max_nq, q_heads, dense, &pl)) return 0;
   const int G = q_heads / kvp->kv_heads;
   const int NR = pl.NR, C = pl.C;
   const bool wide = pl.wide;
@@ -993,6 +1014,7 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
   prm.q_heads = q_heads;
   prm.scale_log2 = scale * LOG2E;
   prm.chunk = pl.chunk;
+  prm.dense = dense;
   static const int trace = env_int("SD_ATTN_TRACE", 0);
   prm.trace = trace;
   *handled = true;

@@ -140,6 +140,7 @@ struct Params {
   int q_heads;
   float scale_log2;
   int chunk;  // keys per CTA, multiple of TK
+  int dense;  // 1: items have no critical list and pages >= 16 tokens (page ids staged, not slots)
 };
 
 // (m, l) softmax-statistics merge
@@ -176,15 +177,17 @@ struct Layout {
   int ring, q, pbuf, pos, slot, bar, wm, wl, xm, xl, rowlse, tptr, total;
 };
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
-// ct = key tiles of this launch's chunk (positions + physical slots are staged per key)
-__host__ __device__ inline Layout make_layout(int NR, int NSLOT, int TMAX, int ct) {
+// ct = key tiles of this launch's chunk.  Gathered (critical-list) items stage a position
+// and a physical slot per key; dense items (dense = 1: no critical list, pages of >= 16
+// tokens) only the chunk's block-table entries, one per page.
+__host__ __device__ inline Layout make_layout(int NR, int NSLOT, int TMAX, int ct, int dense = 0) {
   Layout L{};
   int o = 0;
   L.ring = o;  o += NSLOT * TILE_BYTES;
   L.q = o;     o += 2 * NR * 128;        // [dhalf][NR][128 B], SWIZZLE_128B
   L.pbuf = o;  o += 2 * NR * TK * 2;     // 2 x P^T [128 keys][NR] bf16, MN-major, no swizzle
-  L.pos = o;   o += ct * TK * 4;
-  L.slot = o;  o += ct * TK * 4;
+  L.pos = o;   o += dense ? (ct * TK / 16 + 2) * 4 : ct * TK * 4;
+  L.slot = o;  o += dense ? 0 : ct * TK * 4;
   o = align_up(o, 8);
   L.bar = o;   o += (2 * NSLOT + 2 * TMAX + 5) * 8;
   L.wm = o;    o += NSW * NR * 4;

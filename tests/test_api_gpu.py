@@ -146,3 +146,54 @@ def test_bf16_mode_runs_and_is_lossless_vs_own_greedy():
     committed, stats = E.decode_to_completion(model, E.DecodeRequest(0, prompt, 48), 4, 0.25)
     assert len(committed) == 48
     assert stats.realized_alpha > 0.5
+
+
+@pytest.mark.parametrize("planted", [None, [2, 40, 77]])
+def test_native_layer_loop_matches_python_loop_bf16(planted):
+    """sd_forward_layers (the bf16 layer stack issued from C++: cuBLAS GEMMs, norms, K5,
+    K1/K2) == the same stack issued op by op from Python (torch GEMMs), on a mixed batch
+    of verify rows (score capture) and draft rows (critical list + fresh tail)."""
+    from paper_2512_01278_b200.model import AttnLaunch, forward_rows, lm_head, make_items
+    from paper_2512_01278_b200.paged import PagedKvPool
+
+    cfg = M.ModelConfig(3, 16, 4, 128, 1024, seed=5)  # Hq 16, Hkv 4 (GQA 4), d 128
+    model = M.init_model(cfg, dtype=torch.bfloat16)
+    if planted:
+        model = M.plant_attention_concentration(model, planted)
+    dev = model.device
+    rng = np.random.default_rng(0)
+    n0 = 300
+    results = []
+    for native in (True, False):
+        pool = PagedKvPool(cfg.num_layers, cfg.num_kv_heads, cfg.head_dim, 64, 16, 2, 32, torch.bfloat16, dev)
+        for r in range(2):
+            pool.ensure_tokens(r, n0 + 8)
+        pool.sync_table()
+        g = torch.Generator(device=dev).manual_seed(1)
+        pool.k.copy_(torch.randn(pool.k.shape, generator=g, device=dev))
+        pool.v.copy_(torch.randn(pool.v.shape, generator=g, device=dev))
+        # request 0 verifies 5 tokens at n0..n0+4; request 1 drafts 1 token at n0+2 over a critical list
+        toks = torch.tensor(rng.integers(0, 1024, 6), dtype=torch.int32, device=dev) if not results else results[0][3]
+        rt = torch.tensor([0] * 5 + [1], dtype=torch.int32, device=dev)
+        rp = torch.tensor([n0 + i for i in range(5)] + [n0 + 2], dtype=torch.int32, device=dev)
+        crit = torch.tensor(sorted(rng.choice(n0, 20, replace=False).tolist()) if not results else results[0][4],
+                            dtype=torch.int32, device=dev)
+        acc = torch.zeros(5, n0 + 8, dtype=torch.float32, device=dev)
+        launches = [AttnLaunch(make_items([(0, 0, 5, n0, 0, 0, 0, 0, 1)], dev), 1, n0 + 5, 5, acc=acc,
+                               acc_row_stride=n0 + 8),
+                    AttnLaunch(make_items([(1, 5, 1, n0 + 2, 0, 20, n0, -1, 0)], dev), 1, 23, 1, crit=crit)]
+        old = M.NATIVE_FORWARD
+        M.NATIVE_FORWARD = native
+        try:
+            x = forward_rows(model, pool, toks, rt, rp, launches)
+        finally:
+            M.NATIVE_FORWARD = old
+        logits = lm_head(model, x)
+        torch.cuda.synchronize()
+        kk, _ = pool.read(0, range(n0, n0 + 5))
+        results.append((logits.float().cpu(), acc.cpu(), kk.float().cpu(), toks, crit.tolist()))
+    (ln, an, kn, _, _), (lp, ap, kp, _, _) = results
+    scale = lp.abs().max().item()
+    assert (ln - lp).abs().max().item() <= 2e-2 * max(1.0, scale)
+    assert (an - ap).abs().max().item() <= 2e-2 * 16
+    assert (kn - kp).abs().max().item() <= 2e-2 * max(1.0, kp.abs().max().item())

@@ -65,7 +65,7 @@ def parse():
     p.add_argument("--k", type=int, default=4)
     p.add_argument("--sparsity", type=float, default=0.05)
     p.add_argument("--layers", type=int, default=C1["layers"])
-    p.add_argument("--variants", default="planted", help="comma list of extra variants: planted,sweep,none")
+    p.add_argument("--variants", default="planted", help="comma list of extra variants: planted (alpha ~ 1), c3 (configs[3] 32B-shaped), none")
     p.add_argument("--pool", choices=["full", "window"], default="full")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-layers", type=int, default=None)
@@ -155,14 +155,14 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     max_seq = args.prompt + args.output if args.pool == "full" else ctx + 64
     results = {}
 
-    def build_decoder(m):
+    def build_decoder(m, B=B, ctx=ctx, max_seq=max_seq):
         dec = BatchedDecoder(m, k, s, max_requests=B, max_seq_len=max_seq)
         # shard: global request ids rank*B .. rank*B+B-1 (independent units, no collective)
         reqs = []
         for i in range(B):
             rid = rank * B + i
-            prompt = synthetic_prompt(0, rid, args.prompt, cfg.vocab_size)
-            cont = synthetic_prompt(1, rid, ctx - args.prompt, cfg.vocab_size)
+            prompt = synthetic_prompt(0, rid, args.prompt, m.config.vocab_size)
+            cont = synthetic_prompt(1, rid, ctx - args.prompt, m.config.vocab_size)
             reqs.append(DecodeRequest(rid, prompt + cont, max_seq - ctx))
         seqs = dec.prefill(reqs, max_rows=32768)
         buckets = PhaseBuckets.empty(k)
@@ -180,11 +180,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         batch, _ = form_batch(cands, [], PipelineMode.SYNCHRONOUS)
         return dec.step(batch.draft_members, batch.verify_members)
 
-    def measure(m, steps, warmup, label, with_roofline):
+    def measure(m, steps, warmup, label, with_roofline, **dims):
         """Warm up, then time `steps` iterations with NOTHING but the iterations in the
         timed region (no per-launch events); afterwards, if asked, run a few more
         iterations with per-launch CUDA events on the K1 / K2 launches for the roofline."""
-        dec = build_decoder(m)
+        dec = build_decoder(m, **dims)
         torch.cuda.synchronize()
         for _ in range(warmup):
             one_iteration(dec)
@@ -243,7 +243,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
             dec.attn_timer = timer
             # algorithmic bytes of each iteration's K1/K2 launches, from
             # the host-side batch plan right before the step
-            Hkv, Hq, d, L = cfg.num_kv_heads, cfg.num_q_heads, cfg.head_dim, cfg.num_layers
+            mc = m.config
+            Hkv, Hq, d, L = mc.num_kv_heads, mc.num_q_heads, mc.head_dim, mc.num_layers
             Pb = 2 * d * 2
             for _ in range(min(steps, 6)):
                 vb = db = 0
@@ -272,9 +273,24 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     main = measure(model, args.steps, args.warmup, "random", True)
     variants = {}
     extra = [v for v in args.variants.split(",") if v and v != "none"]
+    planted = None
     if "planted" in extra:
         planted = sd.plant_attention_concentration(model, list(range(5, args.prompt, args.prompt // 12))[:12])
         variants["planted_s0.05"] = measure(planted, max(3, args.steps // 2), 2, "planted", False)
+    if "c3" in extra:
+        # configs[3]: Qwen3-32B-shaped (oracle family: h = 64 x 128, GQA 8), 32K output,
+        # batch 64 over 8 GPUs = 8 requests per GPU, mid-run context 512 + 16384
+        model = planted = None  # the 8B-shaped weights (shared by the planted view) are not needed
+        torch.cuda.empty_cache()
+        c3cfg = sd.ModelConfig(64, 64, 8, 128, C1["vocab"], seed=0)
+        m3 = sd.init_model(c3cfg, dtype=torch.bfloat16, device=dev, fast_init=True)
+        c3out = 32768
+        v = measure(m3, max(3, args.steps // 2), 3, "c3", True, B=8, ctx=args.prompt + c3out // 2,
+                    max_seq=args.prompt + c3out)
+        v["workload"] = ("configs[3]: Qwen3-32B-shaped (L=64, Hq=64, Hkv=8, d=128) random-init bf16, 8 requests "
+                         "per GPU (batch 64 over 8 GPUs), prompt 512, output 32768, mid-run context 16896")
+        variants["configs3_32b"] = v
+        del m3
 
     # gather: tokens summed, time = max over ranks (device clock)
     vals = torch.tensor([main["emitted"], main["dev_s"], main["wall_s"]], dtype=torch.float64, device=dev)
@@ -441,6 +457,13 @@ def main():
         variants = {}
         for name, v in res["variants"].items():
             variants[name] = {"value": v["total_emitted"] / v["dev_s_max"], "unit": "tokens/s", "alpha": v["alpha"]}
+            if v.get("workload"):
+                variants[name]["workload"] = v["workload"]
+                variants[name]["ms_per_step"] = v["dev_s_max"] / max(3, args.steps // 2) * 1000.0
+            if v.get("verify_ms_total"):
+                variants[name]["verify_gbs"] = v["verify_bytes"] / (v["verify_ms_total"] / 1000.0) / 1e9
+            if v.get("draft_ms_total"):
+                variants[name]["draft_gbs"] = v["draft_bytes"] / (v["draft_ms_total"] / 1000.0) / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["dev_s"] / args.steps * 1000.0, "higher_is_better": True,

@@ -146,12 +146,13 @@ int sd_greedy_accept(const int32_t* targets, const int32_t* tokens, const int32_
 int sd_rmsnorm_cast(const float* x, int32_t rows, int32_t h, float eps, void* out, int32_t out_dtype,
                     void* stream);
 
-/* One layer's bf16 weights, row-major [in][out] (model.py:77-105). */
+/* One layer's bf16 weights (model.py:77-105), each stored out-major [out][in]
+ * (nn.Linear layout; the reference's [in][out] matrix transposed). */
 typedef struct sd_layer_weights {
-  const void* w_qkv;   /* [h][(q_heads + 2 kv_heads) d] = [wq | wk | wv] */
+  const void* w_qkv;   /* [(q_heads + 2 kv_heads) d][h]: rows of wq, then wk, then wv */
   const void* wo;      /* [h][h]   */
-  const void* mlp_in;  /* [h][2h]  */
-  const void* mlp_out; /* [2h][h]  */
+  const void* mlp_in;  /* [2h][h]  */
+  const void* mlp_out; /* [h][2h]  */
 } sd_layer_weights;
 
 /* One sd_attention launch per layer (arguments as in sd_attention). */

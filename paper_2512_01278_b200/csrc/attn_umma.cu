@@ -38,7 +38,7 @@ namespace sd {
 namespace umma_attn {
 
 template <int G, int NR, int NSLOT, int TCOLS>
-__global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(const Params p) {
+__device__ __forceinline__ void verify_body(const Params& p, const int h, const int item_idx) {
   constexpr int TMAX = (TCOLS - NR) / NR;  // S tiles resident in TMEM (slot ring)
   constexpr int OCOL = TMAX * NR;          // O^T accumulator columns
   constexpr int NTOK = NR / G;             // token slots covered by NR rows
@@ -46,8 +46,7 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
   cg::cluster_group cluster = cg::this_cluster();
   const int C = static_cast<int>(cluster.num_blocks());
   const int crank = static_cast<int>(cluster.block_rank());
-  const int h = blockIdx.y;
-  const Item it = load_item(p.items, blockIdx.z);
+  const Item it = load_item(p.items, item_idx);
   const int R = it.nq * G;
   const int Nk = it.num_keys();
   const int kb = crank * p.chunk;
@@ -480,6 +479,11 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
 #undef TRACE
 }
 
+template <int G, int NR, int NSLOT, int TCOLS>
+__global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(const Params p) {
+  verify_body<G, NR, NSLOT, TCOLS>(p, blockIdx.y, blockIdx.z);
+}
+
 // ---------------------------------------------------------------------------------------
 // Head-packed draft kernel (K1, one query token per item): a CTA covers HPC kv heads of one
 // item, and a 128-row UMMA tile is KPT = 128 / HPC keys x HPC heads (head-major rows), so
@@ -527,7 +531,7 @@ __host__ __device__ inline Layout make_hp_layout(int NR, int NSLOT, int TMAX, in
 }
 
 template <int G, int HPC, int NSLOT, int TCOLS>
-__global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_hp_kernel(const Params p) {
+__device__ __forceinline__ void draft_body(const Params& p, const int hgroup, const int item_idx) {
   constexpr int NQ = HPC * G;                       // q heads of the CTA
   constexpr int NR = NQ < 16 ? 16 : NQ;             // UMMA N
   constexpr int KPT = TK / HPC;                     // keys per tile
@@ -536,8 +540,8 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_hp_kernel(
   constexpr int WH = KPT >= 32 ? 1 : 32 / KPT;      // heads per warp (rows of a warp)
   static_assert(KPT == 16 || KPT == 32, "head packing: 4 or 8 heads per CTA");
 
-  const int h0 = blockIdx.x * HPC;
-  const Item it = load_item(p.items, blockIdx.y);
+  const int h0 = hgroup * HPC;
+  const Item it = load_item(p.items, item_idx);
   const int nk = it.num_keys();
   const int nt = (nk + KPT - 1) / KPT;
   const int TR = min(nt, TMAX);
@@ -814,6 +818,29 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_hp_kernel(
 }
 
 template <int G, int HPC, int NSLOT, int TCOLS>
+__global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_hp_kernel(const Params p) {
+  draft_body<G, HPC, NSLOT, TCOLS>(p, blockIdx.x, blockIdx.y);
+}
+
+// f3: one launch for a layer's verify (K2) and draft (K1) work.  The grid holds the verify
+// clusters first (blockIdx.z < nv: unit z = item z / Hkv, head z % Hkv, chunk = cluster
+// rank) and then clusters of C head-packed draft CTAs (no cluster cooperation among them),
+// so the block scheduler fills the verify launch's tail wave with draft work instead of
+// running the drafts as a separate, under-filled launch.
+template <int G, int NRV, int NSLOT, int TCOLS>
+__global__ void __launch_bounds__(NT, 2) attn_fused_kernel(const Params pv, const Params pd, int nv, int nd) {
+  const int z = blockIdx.z;
+  if (z < nv) {
+    verify_body<G, NRV, NSLOT, TCOLS>(pv, z % pv.kv.kv_heads, z / pv.kv.kv_heads);
+    return;
+  }
+  const int dc = (z - nv) * gridDim.x + blockIdx.x;
+  if (dc >= nd) return;
+  const int groups = pd.kv.kv_heads / 4;
+  draft_body<G, 4, NSLOT, TCOLS>(pd, dc % groups, dc / groups);
+}
+
+template <int G, int HPC, int NSLOT, int TCOLS>
 int launch_hp(const Params& prm, int num_items, int kv_heads, int ct, cudaStream_t stream) {
   constexpr int NQ = HPC * G, NR = NQ < 16 ? 16 : NQ, TMAX = (TCOLS - NR) / NR;
   auto kern = attn_umma_hp_kernel<G, HPC, NSLOT, TCOLS>;
@@ -1026,6 +1053,93 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
   SD_UMMA_CASE(4, 16) SD_UMMA_CASE(4, 32) SD_UMMA_CASE(4, 48) SD_UMMA_CASE(4, 64)
   SD_UMMA_CASE(8, 16) SD_UMMA_CASE(8, 32) SD_UMMA_CASE(8, 48) SD_UMMA_CASE(8, 64)
 #undef SD_UMMA_CASE
+  *handled = false;
+  return 0;
+}
+
+// f3 fused launch of one layer's verify launch (items_v, K2 with score capture) and draft
+// launch (items_d, K1 over critical lists) when both fit the tcgen05 kernels; otherwise
+// *handled = false and the caller issues the two launches separately.
+int launch_attn_fused(const void* q, void* out, const sd_paged_kv* kvp, int layer, const int32_t* items_v,
+                      int nv_items, int v_max_keys, int v_max_nq, float* acc, int64_t acc_stride,
+                      const int32_t* items_d, int nd_items, int d_max_keys, const int32_t* crit,
+                      const int32_t* planted, int n_planted, float bonus, int q_heads, float scale,
+                      cudaStream_t stream, bool* handled) {
+  using namespace umma_attn;
+  *handled = false;
+  // measured: device-only configs[1] forward 8.52 ms fused vs 8.30 ms as two launches (the
+  // draft CTAs queue behind the verify clusters instead of filling their tail): off by default
+  static const int enable = env_int("SD_ATTN_FUSED", 0);
+  const int G = q_heads / kvp->kv_heads;
+  if (!enable || nv_items == 0 || nd_items == 0 || v_max_nq < 2) return 0;
+  if (kvp->dtype != SD_DTYPE_BF16 || kvp->head_dim != D || !(G == 4 || G == 8) || kvp->kv_heads % 4 != 0) return 0;
+  UmmaPlan pl;
+  const int dense = kvp->page_shift >= 4 ? 1 : 0;
+  if (!umma_plan(kvp, nv_items, v_max_keys, v_max_nq, q_heads, dense, &pl) || pl.wide || pl.NR > 48) return 0;
+  const int NRD = 4 * G, tmax_d = (256 - NRD) / NRD;
+  const int ct_tiles = (max(d_max_keys, 1) + 31) / 32;
+  const int ct_d = (ct_tiles * 32 + TK - 1) / TK;
+  if (ct_tiles > tmax_d) return 0;
+  const int tmax_v = (256 - pl.NR) / pl.NR;
+  const int smem = max(make_layout(pl.NR, 2, tmax_v, pl.chunk / TK, dense).total, make_hp_layout(NRD, 2, tmax_d, ct_d).total);
+  if (smem > 113 * 1024) return 0;
+  static const int trace = env_int("SD_ATTN_TRACE", 0);
+  if (trace) return 0;
+  Params pv{}, pd{};
+  for (Params* pp : {&pv, &pd}) {
+    pp->q = static_cast<const __nv_bfloat16*>(q);
+    pp->out = static_cast<__nv_bfloat16*>(out);
+    pp->lse_out = nullptr;
+    pp->kv = make_paged(kvp);
+    pp->layer = layer;
+    pp->planted = planted;
+    pp->n_planted = n_planted;
+    pp->bonus_log2 = bonus * LOG2E;
+    pp->q_heads = q_heads;
+    pp->scale_log2 = scale * LOG2E;
+  }
+  pv.items = items_v, pv.acc = acc, pv.acc_stride = acc_stride, pv.chunk = pl.chunk, pv.dense = dense;
+  pd.items = items_d, pd.crit = crit, pd.chunk = ct_d * TK;
+  const int C = pl.C;
+  const int nv = nv_items * kvp->kv_heads;
+  const int nd = nd_items * (kvp->kv_heads / 4);
+  const int nz = nv + (nd + C - 1) / C;
+  auto go = [&](auto kern) -> int {
+    static int configured = 0;
+    if (smem > configured) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      configured = smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C, 1, nz);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, pv, pd, nv, nd);
+    count_launch();
+    if (e != cudaSuccess) {
+      set_error(std::string("sd_attention (fused draft + verify) launch: ") + cudaGetErrorString(e));
+      return (int)e;
+    }
+    return 0;
+  };
+  *handled = true;
+  if (G == 4) {
+    if (pl.NR == 16) return go(attn_fused_kernel<4, 16, 2, 256>);
+    if (pl.NR == 32) return go(attn_fused_kernel<4, 32, 2, 256>);
+    return go(attn_fused_kernel<4, 48, 2, 256>);
+  }
+  if (pl.NR == 32) return go(attn_fused_kernel<8, 32, 2, 256>);
+  if (pl.NR == 48) return go(attn_fused_kernel<8, 48, 2, 256>);
   *handled = false;
   return 0;
 }

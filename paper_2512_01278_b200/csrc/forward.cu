@@ -29,6 +29,12 @@ extern "C" int sd_attention(const void* q, void* out, float* lse, const sd_paged
 
 namespace sd {
 
+int launch_attn_fused(const void* q, void* out, const sd_paged_kv* kvp, int layer, const int32_t* items_v,
+                      int nv_items, int v_max_keys, int v_max_nq, float* acc, int64_t acc_stride,
+                      const int32_t* items_d, int nd_items, int d_max_keys, const int32_t* crit,
+                      const int32_t* planted, int n_planted, float bonus, int q_heads, float scale,
+                      cudaStream_t stream, bool* handled);
+
 __global__ void tanh_bf16_kernel(__nv_bfloat16* x, int64_t n) {
   int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
   const int64_t step = (int64_t)gridDim.x * blockDim.x * 8;
@@ -55,12 +61,14 @@ static cublasHandle_t handle_for_thread() {
   return h;
 }
 
-// row-major C[R x N] (+)= A[R x K] . B[K x N]; A, B bf16, C bf16 or fp32 (beta = 0 / 1)
-static int gemm(cublasHandle_t hd, int R, int N, int K, const void* A, const void* B, void* C, bool c_f32,
+// row-major C[R x N] (+)= A[R x K] . W with W stored [N][K] (out-major, nn.Linear layout):
+// column-major C^T = op_T(W) . A^T, i.e. cuBLAS's TN form.  A, W bf16; C bf16 or fp32
+// (beta = 0 / 1)
+static int gemm(cublasHandle_t hd, int R, int N, int K, const void* A, const void* Wt, void* C, bool c_f32,
                 float beta) {
   const float alpha = 1.f;
   const cublasStatus_t st =
-      cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_N, N, R, K, &alpha, B, CUDA_R_16BF, N, A, CUDA_R_16BF, K, &beta, C,
+      cublasGemmEx(hd, CUBLAS_OP_T, CUBLAS_OP_N, N, R, K, &alpha, Wt, CUDA_R_16BF, K, A, CUDA_R_16BF, K, &beta, C,
                    c_f32 ? CUDA_R_32F : CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
   if (st != CUBLAS_STATUS_SUCCESS) {
     set_error("sd_forward_layers: cublasGemmEx failed (" + std::to_string((int)st) + ")");
@@ -92,7 +100,16 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
     if ((rc = sd_rmsnorm_cast(x, rows, hidden, eps, hn, SD_DTYPE_BF16, stream)) != 0) return rc;
     if ((rc = sd::gemm(hd, rows, qkv_w, hidden, hn, w[l].w_qkv, qkv, false, 0.f)) != 0) return rc;
     if ((rc = sd_rope_kv_write(qkv, qkv_w, rows, row_table, row_pos, kv, l, q_heads, q, stream)) != 0) return rc;
-    for (int i = 0; i < num_launches; ++i) {
+    bool fused = false;
+    if (num_launches == 2 && launches[0].max_nq > 1 && launches[1].max_nq == 1) {  // f3: verify + draft
+      const sd_attn_launch& v = launches[0];
+      const sd_attn_launch& d = launches[1];
+      rc = sd::launch_attn_fused(q, ctx, kv, l, v.items, v.num_items, v.max_keys, v.max_nq, v.acc, v.acc_row_stride,
+                                 d.items, d.num_items, d.max_keys, d.crit, planted, num_planted, planted_bonus,
+                                 q_heads, scale, s, &fused);
+      if (rc != 0) return rc;
+    }
+    for (int i = 0; i < num_launches && !fused; ++i) {
       const sd_attn_launch& a = launches[i];
       if (a.num_items == 0) continue;
       if ((rc = sd_attention(q, ctx, nullptr, kv, l, a.items, a.num_items, a.max_keys, a.max_nq, a.crit, a.acc,

@@ -90,7 +90,8 @@ class LayerWeights:
 
 
 class ToyModel:
-    """Device-resident weights.  ``w_qkv[l]`` = [wq | wk | wv] (h, (Hq+2Hkv)d)
+    """Device-resident weights.  ``w_qkv[l]`` = [wq | wk | wv] (h, (Hq+2Hkv)d); every
+    layer matrix is stored [out][in] and exposed as an [in][out] transposed view
     so one GEMM feeds the RoPE/KV-append kernel."""
 
     def __init__(self, config: ModelConfig, embedding: torch.Tensor, w_qkv, wo, mlp_in, mlp_out,
@@ -155,12 +156,17 @@ def init_model(config: ModelConfig, dtype: torch.dtype = torch.float32, device="
 
     emb = draw((config.vocab_size, h))
     w_qkv, wo, mlp_in, mlp_out = [], [], [], []
+    def out_major(w: torch.Tensor) -> torch.Tensor:
+        # stored [out][in] (nn.Linear layout: the GEMMs run cuBLAS's TN form), exposed as the
+        # reference's [in][out] matrix through a transposed view (same values)
+        return w.t().contiguous().t()
+
     for _ in range(config.num_layers):
         m = {name: draw(shape) for name, shape in shapes}
-        w_qkv.append(torch.cat([m["wq"], m["wk"], m["wv"]], dim=1).contiguous())
-        wo.append(m["wo"])
-        mlp_in.append(m["mlp_in"])
-        mlp_out.append(m["mlp_out"])
+        w_qkv.append(out_major(torch.cat([m["wq"], m["wk"], m["wv"]], dim=1)))
+        wo.append(out_major(m["wo"]))
+        mlp_in.append(out_major(m["mlp_in"]))
+        mlp_out.append(out_major(m["mlp_out"]))
         del m
     return ToyModel(config, emb, w_qkv, wo, mlp_in, mlp_out)
 

@@ -57,6 +57,12 @@ static cublasHandle_t handle_for_thread() {
   if (h == nullptr) {
     if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
     cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);
+    // a 64 MB workspace lets cuBLAS use split-K kernels for the skinny (M ~ 200) GEMMs;
+    // owned by the handle for the life of the process (SD_CUBLAS_WS_MB, 0 = none)
+    const char* e = getenv("SD_CUBLAS_WS_MB");
+    const size_t mb = e && *e ? (size_t)atoi(e) : 64;
+    void* ws = nullptr;
+    if (mb > 0 && cudaMalloc(&ws, mb << 20) == cudaSuccess) cublasSetWorkspace(h, ws, mb << 20);
   }
   return h;
 }

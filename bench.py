@@ -65,7 +65,9 @@ def parse():
     p.add_argument("--k", type=int, default=4)
     p.add_argument("--sparsity", type=float, default=0.05)
     p.add_argument("--layers", type=int, default=C1["layers"])
-    p.add_argument("--variants", default="planted", help="comma list of extra variants: planted (alpha ~ 1), c3 (configs[3] 32B-shaped), none")
+    p.add_argument("--variants", default="planted,sweep",
+                   help="comma list of extra variants: planted (alpha ~ 1), sweep (s = 1/2/10%%), c3 (configs[3] "
+                        "32B-shaped), none")
     p.add_argument("--pool", choices=["full", "window"], default="full")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-layers", type=int, default=None)
@@ -277,6 +279,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     if "planted" in extra:
         planted = sd.plant_attention_concentration(model, list(range(5, args.prompt, args.prompt // 12))[:12])
         variants["planted_s0.05"] = measure(planted, max(3, args.steps // 2), 2, "planted", False)
+    if "sweep" in extra:
+        # configs[1] names a PillarAttn top-k budget sweep: the same workload at other s
+        base_s = s
+        for sv in (0.01, 0.02, 0.10):
+            s = sv  # build_decoder reads s from this scope
+            variants[f"budget_s{sv:g}"] = measure(model, max(3, args.steps // 4), 3, f"s{sv:g}", False)
+        s = base_s
     if "c3" in extra:
         # configs[3]: Qwen3-32B-shaped (oracle family: h = 64 x 128, GQA 8), 32K output,
         # batch 64 over 8 GPUs = 8 requests per GPU, mid-run context 512 + 16384

@@ -911,11 +911,15 @@ static int chunk_cap_tiles(int NR, int nslot, int tmax, int budget, int dense) {
 // (32 KB fills per CTA + fixed per-CTA cost ~7 fills, fitted to traced C sweeps).  Chunks longer than the TMEM-resident
 // tiles re-read the evicted tiles' K in phase 2 (fills = 3*ct - tmax).
 static bool plan_umma(int max_keys, int num_items, int kv_heads, int tmax, int cap, int slots, int* C_out,
-                      int* chunk_out) {
+                      int* chunk_out, int dense) {
   using namespace umma_attn;
   const int tiles = (max_keys + TK - 1) / TK;
   static const int force_c = env_int("SD_ATTN_C", 0);
-  static const double ovh = env_int("SD_UMMA_OVH10", 70) / 10.0;
+  // fixed per-CTA cost in fills: ~7 for dense verify chunks (traced C sweeps); re-reading an
+  // evicted tile of a gathered (critical-list) chunk costs a second gather, so gathered
+  // launches weight the per-CTA cost less and avoid re-reads
+  static const double ovh_dense = env_int("SD_UMMA_OVH10", 70) / 10.0;
+  const double ovh = dense ? ovh_dense : 2.0;
   const long long work = (long long)num_items * kv_heads;
   int best = 0;
   double best_cost = 1e300;
@@ -957,9 +961,9 @@ static bool umma_plan(const sd_paged_kv* kvp, int num_items, int max_keys, int m
   int C = 1, chunk = TK;
   bool wide = false;
   if (!(wide_env != 1 && narrow_cap > 0 &&
-        plan_umma(mk, num_items, kvp->kv_heads, (256 - NR) / NR, narrow_cap, 296, &C, &chunk))) {
+        plan_umma(mk, num_items, kvp->kv_heads, (256 - NR) / NR, narrow_cap, 296, &C, &chunk, dense))) {
     if (wide_env == 0 || wide_cap == 0 ||
-        !plan_umma(mk, num_items, kvp->kv_heads, (512 - NR) / NR, wide_cap, 148, &C, &chunk))
+        !plan_umma(mk, num_items, kvp->kv_heads, (512 - NR) / NR, wide_cap, 148, &C, &chunk, dense))
       return false;
     wide = true;
   }

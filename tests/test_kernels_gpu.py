@@ -255,6 +255,49 @@ def test_sparse_draft_attention_large_budget_bf16():
     assert np.abs(lse.double().cpu().numpy() - rl).max() <= 2e-2
 
 
+def test_verify_mixed_token_counts_short_contexts_bf16():
+    """One launch mixing 1..5-token verify items (first-round round targets) over short
+    contexts (0 .. 1000 committed keys, tile and page boundaries), planted bias on."""
+    rng = np.random.default_rng(21)
+    Hkv, G, d = 8, 4, 128
+    Hq = Hkv * G
+    cases = [(0, 2), (1, 5), (127, 3), (128, 1), (129, 5), (1000, 4)]  # (n0, tokens)
+    maxn = max(n + t for n, t in cases)
+    pool = _pool(1, Hkv, d, maxn, len(cases), torch.bfloat16, shuffle_seed=13)
+    for r, (n, t) in enumerate(cases):
+        _fill(pool, r, n + t, rng)
+    rows, q0 = [], 0
+    for r, (n, t) in enumerate(cases):
+        rows.append((r, q0, t, n, 0, 0, 0, r * 5, 1))
+        q0 += t
+    items = make_items(rows, DEV)
+    q = torch.from_numpy(rng.normal(size=(q0, Hq, d))).to(DEV, torch.bfloat16)
+    out = torch.empty_like(q)
+    lse = torch.empty(q0, Hq, dtype=torch.float32, device=DEV)
+    acc = torch.zeros(len(cases) * 5, maxn, dtype=torch.float32, device=DEV)
+    planted = (5, 128, 1001)
+    K.attention(q, out, pool, 0, items, len(cases), maxn, 5, Hq, lse=lse, acc=acc, acc_row_stride=maxn,
+                planted=torch.tensor(planted, dtype=torch.int32, device=DEV), planted_bonus=1.5)
+    torch.cuda.synchronize()
+    q0 = 0
+    for r, (n, t) in enumerate(cases):
+        kr, vr = pool.read(r, range(n + t))
+        kr, vr = kr.double().cpu().numpy()[:, 0], vr.double().cpu().numpy()[:, 0]
+        qs = q[q0:q0 + t].double().cpu().numpy()
+        ro, rl, ra = _ref_rows(qs, kr, vr, Hq, Hkv, d, [], range(n + t), n, planted=planted, bonus=1.5)
+        assert np.abs(out[q0:q0 + t].double().cpu().numpy() - ro).max() <= 2e-2
+        assert np.abs(lse[q0:q0 + t].double().cpu().numpy() - rl).max() <= 2e-2
+        a = acc[r * 5:r * 5 + t].double().cpu().numpy()
+        for tk in range(t):
+            want = np.zeros(maxn)
+            for p_, val in ra[tk].items():
+                want[p_] = val
+            assert np.abs(a[tk] - want).max() <= 2e-2
+        if t < 5:
+            assert acc[r * 5 + t:r * 5 + 5].abs().max().item() == 0.0  # rows of absent tokens untouched
+        q0 += t
+
+
 def test_topk_golden_kats(golden_topk):
     n = len([k for k in golden_topk if k.endswith(".values")])
     for dt in (torch.float64,):

@@ -157,6 +157,9 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
   tc_fence_after();
   const uint32_t tbase = *tptr;
   if (tid == 0) TRACE(1, gtime());
+  // barrier 0 (C > 1): every peer of the cluster has started before anyone touches its shared
+  // memory (the statistics push below); arrived here, waited right before the first DSMEM use
+  if (C > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
 
   const int64_t row_stride = (int64_t)p.kv.kv_heads * D;  // elements between consecutive slots
   const __nv_bfloat16* Kg = static_cast<const __nv_bfloat16*>(p.kv.k) + (int64_t)p.layer * p.kv.layer_stride + h * D;
@@ -187,12 +190,18 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
       cp_async_mbar_arrive(full + s);
       if (f == nt - 1) {
         if (lane == 0) TRACE(11, gtime());
-        if (C > 1) cluster_arrive();  // K streamed; let the exchange proceed
+        if (C > 1) {
+          cluster_wait();    // barrier 0
+          cluster_arrive();  // barrier 1: K streamed; let the exchange proceed
+        }
       }
     }
     if (lane == 0) TRACE(7, gtime());
     if (C > 1) {
-      if (nt == 0) cluster_arrive();
+      if (nt == 0) {
+        cluster_wait();  // barrier 0
+        cluster_arrive();
+      }
       cluster_wait();
       for (int b = 0; b < 2; ++b) {  // the softmax warps' epilogue barriers
         cluster_arrive();
@@ -232,7 +241,10 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
     };
     for (int t = 0; t < nt; ++t) qk(t, f % NSLOT);
     if (lane == 0) TRACE(10, gtime());
-    if (C > 1) cluster_arrive();  // barrier 1: this warp's part of phase 1 is issued
+    if (C > 1) {
+      cluster_wait();    // barrier 0
+      cluster_arrive();  // barrier 1: this warp's part of phase 1 is issued
+    }
     for (int i2 = 0; i2 < nt; ++i2) {
       if (i2 >= TR) qk(nt + (i2 - TR), f % NSLOT);  // evicted tile: recompute its logits
       const int s = f % NSLOT;
@@ -332,6 +344,7 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
     }
   }
   sw_bar();
+  if (C > 1) cluster_wait();  // barrier 0: all peers have started (DSMEM pushes follow)
   if (tid < R) {
     float mm = -INFINITY, ll = 0.f;
 #pragma unroll

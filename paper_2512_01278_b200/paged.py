@@ -91,7 +91,41 @@ class PagedKvPool:
 
     def release_row(self, row: int) -> None:
         for p in reversed(self._rows.pop(row, [])):
-            self._free.append(p)
+            if p >= 0:
+                self._free.append(p)
+
+    # -- host offload: physical pages leave / rejoin a row ---------------
+    def unmap_pages(self, row: int, logical_pages) -> int:
+        """Return the physical pages behind ``logical_pages`` of ``row`` to the free
+        list (their rows were copied to the host); the block-table entries point at
+        page 0 until remapped, and the row must not be scheduled meanwhile."""
+        pages = self._rows.get(row, [])
+        n = 0
+        for lp in logical_pages:
+            if lp < len(pages) and pages[lp] >= 0:
+                self._free.append(pages[lp])
+                pages[lp] = -1
+                self._table_host[row, lp] = 0
+                n += 1
+        if n:
+            self._dirty.add(row)
+        return n
+
+    def remap_pages(self, row: int, logical_pages) -> int:
+        """Give unmapped ``logical_pages`` of ``row`` fresh physical pages."""
+        pages = self._rows.get(row, [])
+        todo = [lp for lp in logical_pages if lp < len(pages) and pages[lp] < 0]
+        if len(todo) > len(self._free):
+            raise ImpossibleRequestError("device KV pool exhausted while reloading")
+        for lp in todo:
+            pages[lp] = self._free.pop()
+            self._table_host[row, lp] = pages[lp]
+        if todo:
+            self._dirty.add(row)
+        return len(todo)
+
+    def unmapped_pages(self, row: int) -> list:
+        return [i for i, p in enumerate(self._rows.get(row, [])) if p < 0]
 
     def sync_table(self) -> None:
         """Upload dirty block-table rows (host -> device, stream ordered)."""

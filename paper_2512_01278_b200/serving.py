@@ -90,6 +90,9 @@ class BatchedDecoder:
         self.imp = torch.zeros(max_requests, self.acc_w, dtype=torch.float32, device=self.dev)
         self.free_slots = list(range(max_requests - 1, -1, -1))
         self.seqs: dict = {}
+        self._host_kv: dict = {}     # request -> {position: (K rows, V rows)} pinned host copies
+        self.offloaded_bytes = 0
+        self.reloaded_bytes = 0
         self.attn_timer = None       # optional callable(kind, start) for per-launch timing
         self.host_times: list = []   # per step: (host enqueue s, enqueue + device drain s)
         self.last_rows = 0
@@ -116,6 +119,51 @@ class BatchedDecoder:
         s = self.seqs.pop(request_id)
         self.pool.release_row(s.slot)
         self.free_slots.append(s.slot)
+        self._host_kv.pop(request_id, None)
+
+    # -- host offload tier (kvpool.py:213-237,272-311) -----------------
+    def offload_positions(self, request_id, positions) -> int:
+        """Copy the K/V rows of ``positions`` (all layers) to pinned host memory and return
+        every physical page whose tokens are all on the host to the device pool.  The
+        request must not be scheduled until ``reload_positions`` brings them back."""
+        positions = sorted(int(p) for p in positions)
+        s = self.seqs.get(request_id)
+        if s is None or not positions:
+            return 0
+        k, v = self.pool.read(s.slot, positions)  # (n, L, Hkv, d)
+        hk = torch.empty(k.shape, dtype=k.dtype, pin_memory=True)
+        hv = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+        hk.copy_(k, non_blocking=True)
+        hv.copy_(v, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        store = self._host_kv.setdefault(request_id, {})
+        for i, p in enumerate(positions):
+            store[p] = (hk[i], hv[i])
+        ps = self.pool.page_size
+        whole = sorted({p // ps for p in positions if all(q in store for q in range(p // ps * ps, p // ps * ps + ps))})
+        self.pool.unmap_pages(s.slot, whole)
+        self.offloaded_bytes += 2 * k.numel() * k.element_size()
+        return len(positions)
+
+    def reload_positions(self, request_id, positions) -> int:
+        """Inverse of ``offload_positions``: remap pages and copy the rows back."""
+        positions = sorted(int(p) for p in positions)
+        s = self.seqs.get(request_id)
+        store = self._host_kv.get(request_id)
+        if s is None or not positions or store is None:
+            return 0
+        ps = self.pool.page_size
+        self.pool.remap_pages(s.slot, sorted({p // ps for p in positions}))
+        self.pool.sync_table()
+        # a remapped page receives every row it holds: also the still-host rows of pages
+        # that were only partly reloaded stay on the host and are written when they return
+        k = torch.stack([store[p][0] for p in positions])
+        v = torch.stack([store[p][1] for p in positions])
+        self.pool.write(s.slot, positions, k, v)
+        for p in positions:
+            del store[p]
+        self.reloaded_bytes += 2 * k.numel() * k.element_size()
+        return len(positions)
 
     def _emit(self, s: Seq, toks) -> int:
         landed = 0

@@ -167,8 +167,10 @@ def run_token_sim(workload: WorkloadSpec, model_config: ModelConfig, cfg: SimCon
     sim_time = 0.0
     pressure_last = False
     gpu_total = 0.0
+    host_pages: dict = {}  # request -> token pages on the host tier after the last transfer step
 
     def complete(rid):
+        host_pages.pop(rid, None)
         pool.release(rid)
         seq = dec.seqs[rid]
         outputs[rid] = list(seq.committed)
@@ -189,6 +191,17 @@ def run_token_sim(workload: WorkloadSpec, model_config: ModelConfig, cfg: SimCon
         if not lives and waiting[0].arrival_ms > sim_time:
             sim_time = waiting[0].arrival_ms
         pool.step(kv_cfg.capacity_pages, kv_cfg.capacity_pages, allow_reload=not pressure_last)
+        # host tier (kvpool.py:213-237,272-311): the pages the pool moved this iteration
+        # really move; K/V rows of offloaded token pages go to pinned host memory (their
+        # device pages are returned) and come back on reload
+        for rid in list(dec.seqs):
+            now = set(pool.host_pages_of(rid))
+            before = host_pages.get(rid, set())
+            if now - before:
+                dec.offload_positions(rid, now - before)
+            if before - now:
+                dec.reload_positions(rid, before - now)
+            host_pages[rid] = now
         pressure_now = False
         while waiting and waiting[0].arrival_ms <= sim_time and len(lives) < cfg.max_batch:
             req = waiting[0]
@@ -286,6 +299,7 @@ def run_token_sim(workload: WorkloadSpec, model_config: ModelConfig, cfg: SimCon
     else:
         raise SimulationError(f"no completion within {cfg.max_iterations} iterations")
 
+    run_token_sim.last_transfer_bytes = (dec.offloaded_bytes, dec.reloaded_bytes)
     emitted = sum(lv.emitted for lv in finished.values())
     drafted = sum(lv.drafted_total for lv in finished.values())
     accepted = sum(lv.accepted_total for lv in finished.values())

@@ -13,10 +13,13 @@ items over their critical sets), one batched forward, K4 accept, K3 refresh.
 
 The timed window sits at the run's MID-POINT context (prompt 512 + 4096
 already-generated tokens = 4608 KV rows per request): per-iteration cost is
-linear in context, so this equals the mean over the full 8K-output run.  The
-4096 generated tokens are teacher-forced synthetic tokens prefilled through
-the same kernels (scores captured -> first critical set), outside the timed
-region.  KV capacity for the full 8K run is allocated up front.
+linear in context, so this equals the mean over the full 8K-output run.  Setup
+(untimed): the 512-token prompt is prefilled through the model (scores captured);
+the K/V rows of the 4096 teacher-forced continuation tokens are written directly
+as synthetic N(0,1) values (the values change no kernel's work; --real-prefill
+runs them through the model, ~160 s per decoder) and the first critical set is
+selected over all 4608 positions.  KV capacity for the full 8K run is allocated
+up front.
 
 Setup (untimed): prefill, then an 8-iteration pre-roll (first-round phase stagger,
 cuBLAS shape caches), then W warm-up iterations.  The K timed iterations contain
@@ -70,6 +73,8 @@ def parse():
                         "32B-shaped), none")
     p.add_argument("--pool", choices=["full", "window"], default="full")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--real-prefill", action="store_true",
+                   help="prefill the teacher-forced continuation through the model (slow, ~160 s per decoder)")
     p.add_argument("--cpu-sample-layers", type=int, default=None)
     return p.parse_args()
 
@@ -80,58 +85,67 @@ def parse():
 
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event reasons sampled DURING the timed region: NVML polled every
+    ~5 ms from a thread (nvidia-smi's -lms floor is too coarse for a sub-second window)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines: list = []
+        self.samples: list = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thread = None
+        self._nvml = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._pump, daemon=True).start()
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            import pynvml
 
-    def _pump(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - no NVML: report it instead of failing the bench
+            self._nvml = None
+            return
+
+        def run():
+            getr = getattr(self._nvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                self._nvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self._stop.is_set():
+                try:
+                    self.samples.append((self._nvml.nvmlDeviceGetClockInfo(h, self._nvml.NVML_CLOCK_SM), int(getr(h))))
+                except Exception:  # noqa: BLE001
+                    break
+                time.sleep(0.005)
+
+        self._thread = threading.Thread(target=run, daemon=True)
+        self._thread.start()
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if self._nvml is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self._stop.set()
+        self._thread.join(timeout=2)
+        sm = [c for c, _ in self.samples]
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(sm), "how": "NVML every 5 ms during the timed iterations"}
 
 
 # ----------------------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------------------
+
+
+_T0 = time.perf_counter()
+
+
+def log(msg: str) -> None:
+    """Stage timings on stderr (the JSON line is the only stdout output)."""
+    print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
 
 
 def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
@@ -166,7 +180,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
             prompt = synthetic_prompt(0, rid, args.prompt, m.config.vocab_size)
             cont = synthetic_prompt(1, rid, ctx - args.prompt, m.config.vocab_size)
             reqs.append(DecodeRequest(rid, prompt + cont, max_seq - ctx))
-        seqs = dec.prefill(reqs, max_rows=32768)
+        log(f"decoder built (pool {dec.pool.k.numel() * 4 / 1e9:.0f} GB), prefilling {B} x {ctx} tokens")
+        if args.real_prefill:
+            seqs = dec.prefill(reqs, max_rows=32768)
+        else:
+            seqs = dec.prefill_synthetic(reqs, real_tokens=args.prompt, max_rows=32768)
+        torch.cuda.synchronize()
+        log("prefill done")
         buckets = PhaseBuckets.empty(k)
         for sq in seqs:
             sq.round_target = first_round_draft_len(k, assign_new_request(buckets))
@@ -272,19 +292,23 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         torch.cuda.empty_cache()
         return out
 
+    log("model initialised")
     main = measure(model, args.steps, args.warmup, "random", True)
+    log("main measurement done")
     variants = {}
     extra = [v for v in args.variants.split(",") if v and v != "none"]
     planted = None
     if "planted" in extra:
         planted = sd.plant_attention_concentration(model, list(range(5, args.prompt, args.prompt // 12))[:12])
         variants["planted_s0.05"] = measure(planted, max(3, args.steps // 2), 2, "planted", False)
+        log("planted variant done")
     if "sweep" in extra:
         # configs[1] names a PillarAttn top-k budget sweep: the same workload at other s
         base_s = s
         for sv in (0.01, 0.02, 0.10):
             s = sv  # build_decoder reads s from this scope
             variants[f"budget_s{sv:g}"] = measure(model, max(3, args.steps // 4), 3, f"s{sv:g}", False)
+            log(f"budget s={sv:g} done")
         s = base_s
     if "c3" in extra:
         # configs[3]: Qwen3-32B-shaped (oracle family: h = 64 x 128, GQA 8), 32K output,
@@ -462,6 +486,7 @@ def main():
                 traffic = ratio * m["verify_bytes"] / m["verify_launches"]
         cpu = None
         if not args.no_cpu_baseline:
+            log("cpu baseline sample")
             r = cpu_round_sample(args, layers_used=args.cpu_sample_layers)
             cpu = {"value": r["tokens"] / r["seconds"], "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
                    "sample": f"1 draft/verify round (k={args.k} drafts + verify) of one request at context "

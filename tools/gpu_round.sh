@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
-timeout 1500 python bench.py > gpurun_out/bench.log 2>&1
+( time timeout 1500 python bench.py ) > gpurun_out/bench.log 2> gpurun_out/bench_time.log
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1
 timeout 600 python bench_kernels.py --iters 20 > gpurun_out/kb_all.log 2>&1
 timeout 600 python bench_kernels.py --iters 20 --G 8 --ctx 4096,8192,32768 --sparsity 0.05 > gpurun_out/kb_g8.log 2>&1

@@ -14,12 +14,10 @@ items over their critical sets), one batched forward, K4 accept, K3 refresh.
 The timed window sits at the run's MID-POINT context (prompt 512 + 4096
 already-generated tokens = 4608 KV rows per request): per-iteration cost is
 linear in context, so this equals the mean over the full 8K-output run.  Setup
-(untimed): the 512-token prompt is prefilled through the model (scores captured);
-the K/V rows of the 4096 teacher-forced continuation tokens are written directly
-as synthetic N(0,1) values (the values change no kernel's work; --real-prefill
-runs them through the model, ~160 s per decoder) and the first critical set is
-selected over all 4608 positions.  KV capacity for the full 8K run is allocated
-up front.
+(untimed): the 512-token prompt and 4096 teacher-forced continuation tokens are
+prefilled through the same kernels (scores captured -> first critical set; ~10 s
+for 128 requests; --synthetic-prefill writes the continuation's K/V directly
+instead).  KV capacity for the full 8K run is allocated up front.
 
 Setup (untimed): prefill, then an 8-iteration pre-roll (first-round phase stagger,
 cuBLAS shape caches), then W warm-up iterations.  The K timed iterations contain
@@ -73,8 +71,9 @@ def parse():
                         "32B-shaped), none")
     p.add_argument("--pool", choices=["full", "window"], default="full")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--real-prefill", action="store_true",
-                   help="prefill the teacher-forced continuation through the model (slow, ~160 s per decoder)")
+    p.add_argument("--synthetic-prefill", action="store_true",
+                   help="write the teacher-forced continuation's K/V as synthetic values instead of prefilling "
+                        "it through the model (faster setup; same timed work)")
     p.add_argument("--cpu-sample-layers", type=int, default=None)
     return p.parse_args()
 
@@ -181,10 +180,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
             cont = synthetic_prompt(1, rid, ctx - args.prompt, m.config.vocab_size)
             reqs.append(DecodeRequest(rid, prompt + cont, max_seq - ctx))
         log(f"decoder built (pool {dec.pool.k.numel() * 4 / 1e9:.0f} GB), prefilling {B} x {ctx} tokens")
-        if args.real_prefill:
-            seqs = dec.prefill(reqs, max_rows=32768)
-        else:
+        if args.synthetic_prefill:
             seqs = dec.prefill_synthetic(reqs, real_tokens=args.prompt, max_rows=32768)
+        else:
+            seqs = dec.prefill(reqs, max_rows=32768)
         torch.cuda.synchronize()
         log("prefill done")
         buckets = PhaseBuckets.empty(k)

@@ -15,6 +15,7 @@ with the per-member engine calls replaced by one BatchedDecoder.step().
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -29,7 +30,9 @@ from .model import AttnLaunch, ToyModel, forward_rows, lm_head
 from .paged import PagedKvPool
 from .selection import compute_budget
 
-MMA_MAX_ROWS = 80  # rows per K2 work item (query tokens x GQA group) for the tensor-core kernel
+# rows per prefill work item (query tokens x GQA group): <= 64 keeps prefill on the tcgen05
+# kernel (128 x 4608-token prefill: 9.4 s; 80 rows on the mma.sync fallback: 163 s)
+MMA_MAX_ROWS = int(os.environ.get("SD_PREFILL_ROWS", "64"))
 
 
 @dataclass

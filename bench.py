@@ -275,7 +275,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                     if sq.phase == sq.round_target:
                         t = sq.round_target + 1
                         n = sq.n_kv + t
-                        vb += Hkv * n * Pb + 2 * t * Hq * d * 2 + t * n * 4
+                        vb += Hkv * n * Pb + 2 * t * Hq * d * 2 + t * n * 8  # acc: u64 RED per (token, key)
                     else:
                         db += Hkv * (sq.crit_len + sq.phase + 1) * Pb + 4 * sq.crit_len + 2 * Hq * d * 2
                 bytes_acc["verify"] += vb * L

@@ -90,9 +90,11 @@ def main():
         if args.only in ("both", "verify"):
             items = make_items([(r, r * t, t, n, 0, 0, 0, r * t, 1) for r in range(b)], dev)
             W = n + t
-            acc = torch.zeros(b * t, W, device=dev)
-            sec = timeit(lambda l: K.attention(q, out, pool, l, items, b, n + t, t, Hq, acc=acc, acc_row_stride=W))
-            byts = b * (Hkv * (n + t) * Pb + 2 * t * Hq * d * 2 + t * (n + t) * 4)
+            acc = torch.zeros(b * t, W, dtype=torch.int64, device=dev)
+            shift = K.score_shift(1, 36, Hq)
+            sec = timeit(lambda l: K.attention(q, out, pool, l, items, b, n + t, t, Hq, acc=acc, acc_row_stride=W,
+                                               acc_shift=shift))
+            byts = b * (Hkv * (n + t) * Pb + 2 * t * Hq * d * 2 + t * (n + t) * 8)
             flops = 4 * b * t * Hq * (n + t) * d
             print(json.dumps({"kernel": "K2 verify", "ctx": n, "batch": b, "k": k, "G": G, "us": sec * 1e6,
                               "GB/s": byts / sec / 1e9, "frac_hbm": byts / sec / 1e9 / hbm,

@@ -40,10 +40,11 @@
 extern "C" {
 #endif
 
-#define SD_ABI_VERSION 1
+#define SD_ABI_VERSION 2
 
 #define SD_DTYPE_F32 0
 #define SD_DTYPE_BF16 1
+#define SD_DTYPE_F64 2 /* sd_argmax_rows only */
 
 /* Fields of one attention work item (int32 record of SD_ITEM_FIELDS). */
 #define SD_ITEM_TABLE_ROW 0 /* block-table row of the request                      */
@@ -75,6 +76,8 @@ typedef struct sd_paged_kv {
 } sd_paged_kv;
 
 int32_t sd_abi_version(void);
+/* Hash of the sources and build flags the library was compiled from. */
+const char* sd_build_id(void);
 const char* sd_last_error(void);
 /* Number of kernels launched by this process through the library (evidence). */
 int64_t sd_launch_count(void);
@@ -93,33 +96,41 @@ int sd_rope_kv_write(const void* qkv, int64_t qkv_row_stride, int32_t rows,
  *   lse      : [rows][q_heads] float or NULL
  *   items    : device int32 [num_items][SD_ITEM_FIELDS]
  *   crit     : device int32 critical positions (concatenated) or NULL
- *   acc      : float score accumulators; row a has acc_row_stride floats; for
- *              item query token t the row is ACC_ROW + t*ACC_STEP and
- *              acc[row][pos] += sum over the group's q heads of exp(s - lse)
+ *   acc      : uint64 fixed-point score accumulators (one unit = 2^-acc_shift);
+ *              row a has acc_row_stride entries; for item query token t the row
+ *              is ACC_ROW + t*ACC_STEP and
+ *              acc[row][pos] += round(2^acc_shift * sum over the group's q heads
+ *                                     of exp(s - lse))
+ *              Integer addition makes the accumulated value independent of the
+ *              order in which heads, CTAs and layers land (bitwise reproducible).
+ *              Callers pick acc_shift so the largest possible entry (rows summed
+ *              into it x layers x q_heads) stays below 2^62.
  *   planted  : device int32 sorted positions receiving +planted_bonus, or NULL
  *   max_keys, max_nq : host upper bounds over items (launch shaping)
  *   workspace: ZERO-FILLED device scratch of sd_attention_workspace_bytes() bytes;
  *              every call leaves it zero-filled again (reuse it across calls)
- *   flags    : bit0 = force the generic (FFMA) kernel */
+ *   flags    : bit0 = force the generic (FFMA) kernel
+ * bf16 pools with head_dim 128 and GQA group 4 or 8 run the tcgen05 kernels for
+ * items of up to 80 query rows (nq * group); other shapes run the generic kernel. */
 int64_t sd_attention_workspace_bytes(int32_t num_items, int32_t max_keys, int32_t max_nq,
                                      int32_t q_heads, const sd_paged_kv* kv);
 int sd_attention(const void* q, void* out, float* lse, const sd_paged_kv* kv, int32_t layer,
                  const int32_t* items, int32_t num_items, int32_t max_keys, int32_t max_nq,
-                 const int32_t* crit, float* acc, int64_t acc_row_stride,
+                 const int32_t* crit, uint64_t* acc, int64_t acc_row_stride, int32_t acc_shift,
                  const int32_t* planted, int32_t num_planted, float planted_bonus,
                  int32_t q_heads, float scale, void* workspace, int64_t workspace_bytes,
                  int32_t flags, void* stream);
 
-/* K3: per request r: importance[p] = sum_{t < n_rows[r]} acc[r][t][p] for
- * p < kv_len[r]; budget = max(1, min(ceil(s*n - 1e-9), n)) (n = 0 -> 1);
+/* K3: per request r: importance[p] = 2^-acc_shift * sum_{t < n_rows[r]} acc[r][t][p]
+ * (fp64, rows summed in order) for p < kv_len[r]; budget = max(1, min(ceil(s*n - 1e-9), n)) (n = 0 -> 1);
  * crit[r][:] = top-budget positions (value desc, ties to the lower index),
  * ascending; crit_len[r] = min(budget, kv_len[r]).
  * req_index (nullable): request r reads/writes row req_index[r] of acc,
  * importance, crit, crit_len and budget_out (n_rows / kv_len stay indexed by r). */
-int sd_select_critical(const float* acc, int64_t acc_req_stride, int64_t acc_row_stride,
-                       const int32_t* n_rows, const int32_t* kv_len, double sparsity,
+int sd_select_critical(const uint64_t* acc, int64_t acc_req_stride, int64_t acc_row_stride,
+                       int32_t acc_shift, const int32_t* n_rows, const int32_t* kv_len, double sparsity,
                        int32_t num_requests, const int32_t* req_index,
-                       float* importance, int64_t imp_stride,
+                       double* importance, int64_t imp_stride,
                        int32_t* crit, int64_t crit_stride, int32_t* crit_len,
                        int32_t* budget_out, void* stream);
 
@@ -129,7 +140,8 @@ int sd_topk(const void* values, int32_t value_dtype, int64_t stride, const int32
             const int32_t* budget, int32_t num, int32_t* out, int64_t out_stride,
             int32_t* out_len, void* stream);
 
-/* K4a: per-row argmax, ties to the lowest index.  logits [rows][row_stride]. */
+/* K4a: per-row argmax, ties to the lowest index.  logits [rows][row_stride] of
+ * dtype F32, BF16 or F64 (fp64 rows are compared in fp64). */
 int sd_argmax_rows(const void* logits, int32_t dtype, int64_t row_stride, int32_t rows,
                    int32_t vocab, int32_t* out, void* stream);
 
@@ -161,9 +173,9 @@ typedef struct sd_attn_launch {
   int32_t num_items;
   int32_t max_keys;
   int32_t max_nq;
-  int32_t reserved;
+  int32_t acc_shift;
   const int32_t* crit;
-  float* acc;
+  uint64_t* acc;
   int64_t acc_row_stride;
 } sd_attn_launch;
 

@@ -18,8 +18,10 @@ from .model import (KvCache, KVEntry, ModelConfig, ToyModel, forward_full, forwa
                     plant_attention_concentration)
 from .scheduler import (BatchCandidate, IterationBatch, PhaseBuckets, PipelineMode, PipelineSlot, SchedPolicy,
                         assign_new_request, balance_metric, first_round_draft_len, form_batch, step_pipeline)
-from .selection import (AttentionScoreLog, CriticalTokenSet, compute_budget, importance_from_log,
-                        select_critical_tokens)
+from .selection import (AttentionScoreLog, CriticalTokenSet, ScoreRow, aggregate_scores, compute_budget,
+                        importance_from_log, pad_rows, rematerialize_scores, select_critical_tokens)
+from .simulate import KvPoolConfig, SimConfig, SimReport, run_token_sim
+from .workload import ArrivalKind, ArrivalSpec, LengthDist, LengthSpec, SimRequest, WorkloadSpec, generate_workload
 
 try:  # load the in-tree CUDA library eagerly when it has been built
     _native.load_library()
@@ -29,6 +31,9 @@ except ImportError:  # calls into kernels raise loudly until it is built
 __version__ = "0.1.0"
 
 __all__ = [
+    "ArrivalKind", "ArrivalSpec", "KvPoolConfig", "LengthDist", "LengthSpec", "ScoreRow", "SimConfig", "SimReport",
+    "SimRequest", "WorkloadSpec", "aggregate_scores", "generate_workload", "pad_rows", "rematerialize_scores",
+    "run_token_sim",
     "AttentionScoreLog", "BatchCandidate", "CalibrationError", "ConfigurationError", "ContractError",
     "CriticalTokenSet", "DecodeRequest", "DegenerateParameterError", "ImpossibleRequestError", "IterationBatch",
     "KVEntry", "KvCache", "KvPolicy", "KvPool", "ModelConfig", "PhaseBuckets", "PipelineMode", "PipelineSlot",

@@ -43,22 +43,23 @@ class LayerWeights(ctypes.Structure):
 
 class AttnLaunchDesc(ctypes.Structure):
     _fields_ = [("items", ctypes.c_void_p), ("num_items", ctypes.c_int32), ("max_keys", ctypes.c_int32),
-                ("max_nq", ctypes.c_int32), ("reserved", ctypes.c_int32), ("crit", ctypes.c_void_p),
+                ("max_nq", ctypes.c_int32), ("acc_shift", ctypes.c_int32), ("crit", ctypes.c_void_p),
                 ("acc", ctypes.c_void_p), ("acc_row_stride", ctypes.c_int64)]
 
 
 SIGNATURES = {
     "sd_abi_version": (_i32, []),
+    "sd_build_id": (ctypes.c_char_p, []),
     "sd_last_error": (ctypes.c_char_p, []),
     "sd_launch_count": (_i64, []),
     "sd_rope_kv_write": (ctypes.c_int, [_c_p, _i64, _i32, _c_p, _c_p, ctypes.POINTER(PagedKvDesc), _i32, _i32,
                                         _c_p, _c_p]),
     "sd_attention_workspace_bytes": (_i64, [_i32, _i32, _i32, _i32, ctypes.POINTER(PagedKvDesc)]),
     "sd_attention": (ctypes.c_int, [_c_p, _c_p, _c_p, ctypes.POINTER(PagedKvDesc), _i32, _c_p, _i32, _i32, _i32,
-                                    _c_p, _c_p, _i64, _c_p, _i32, ctypes.c_float, _i32, ctypes.c_float, _c_p,
-                                    _i64, _i32, _c_p]),
-    "sd_select_critical": (ctypes.c_int, [_c_p, _i64, _i64, _c_p, _c_p, ctypes.c_double, _i32, _c_p, _c_p, _i64,
-                                          _c_p, _i64, _c_p, _c_p, _c_p]),
+                                    _c_p, _c_p, _i64, _i32, _c_p, _i32, ctypes.c_float, _i32, ctypes.c_float,
+                                    _c_p, _i64, _i32, _c_p]),
+    "sd_select_critical": (ctypes.c_int, [_c_p, _i64, _i64, _i32, _c_p, _c_p, ctypes.c_double, _i32, _c_p, _c_p,
+                                          _i64, _c_p, _i64, _c_p, _c_p, _c_p]),
     "sd_topk": (ctypes.c_int, [_c_p, _i32, _i64, _c_p, _c_p, _i32, _c_p, _i64, _c_p, _c_p]),
     "sd_argmax_rows": (ctypes.c_int, [_c_p, _i32, _i64, _i32, _i32, _c_p, _c_p]),
     "sd_greedy_accept": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i32, _c_p, _c_p, _c_p]),
@@ -70,6 +71,17 @@ SIGNATURES = {
 }
 
 _LIB = None
+ABI_VERSION = 2
+
+
+def source_build_id() -> str | None:
+    """Hash of the CUDA sources + flags the library must have been built from (compiled into
+    the library as sd_build_id()); None when the sources are not shipped."""
+    try:
+        from .csrc import build as B
+    except ImportError:  # pragma: no cover
+        return None
+    return B.source_stamp()
 
 
 def load_library(path: Path | None = None) -> ctypes.CDLL:
@@ -91,8 +103,13 @@ def load_library(path: Path | None = None) -> ctypes.CDLL:
             raise ImportError(f"{p} is stale (missing {name}); rebuild it") from e
         fn.restype = res
         fn.argtypes = args
-    if lib.sd_abi_version() != 1:
+    if lib.sd_abi_version() != ABI_VERSION:
         raise ImportError("libspardec_b200.so ABI version mismatch")
+    want = source_build_id()
+    have = lib.sd_build_id().decode()
+    if want is not None and have != want:
+        raise ImportError(f"{p} was built from other sources (build id {have[:12]} != {want[:12]}); "
+                          "rebuild it with `python -m paper_2512_01278_b200.csrc.build`")
     _LIB = lib
     return lib
 
@@ -120,9 +137,14 @@ def stream_handle() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+SD_DTYPE_F64 = 2
+
+
 def dtype_code(dt: torch.dtype) -> int:
     if dt == torch.float32:
         return SD_DTYPE_F32
+    if dt == torch.float64:
+        return SD_DTYPE_F64
     if dt == torch.bfloat16:
         return SD_DTYPE_BF16
     raise ContractError(f"unsupported dtype {dt}")

@@ -8,18 +8,24 @@ namespace sd {
 
 constexpr int AM_THREADS = 256;
 
-__device__ __forceinline__ void better(float& bv, int& bi, float v, int i) {
+template <typename A>
+__device__ __forceinline__ void better(A& bv, int& bi, A v, int i) {
   if (v > bv || (v == bv && i < bi)) {
     bv = v;
     bi = i;
   }
 }
 
-template <typename T>
+__device__ __forceinline__ double to_acc(double x) { return x; }
+__device__ __forceinline__ float to_acc(float x) { return x; }
+__device__ __forceinline__ float to_acc(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+// T = logits dtype, A = comparison type (fp64 rows compare in fp64: no tie created by rounding)
+template <typename T, typename A>
 __global__ void __launch_bounds__(AM_THREADS) argmax_kernel(const T* __restrict__ logits, int64_t stride,
                                                             int vocab, int32_t* __restrict__ out) {
   const T* row = logits + (int64_t)blockIdx.x * stride;
-  float bv = -INFINITY;
+  A bv = -INFINITY;
   int bi = 0x7fffffff;
   constexpr int VEC = 16 / sizeof(T);
   const bool aligned = (reinterpret_cast<uintptr_t>(row) % 16) == 0;
@@ -30,18 +36,18 @@ __global__ void __launch_bounds__(AM_THREADS) argmax_kernel(const T* __restrict_
       const uint4 raw = reinterpret_cast<const uint4*>(row)[i];
       const T* e = reinterpret_cast<const T*>(&raw);
 #pragma unroll
-      for (int k = 0; k < VEC; ++k) better(bv, bi, to_f(e[k]), i * VEC + k);
+      for (int k = 0; k < VEC; ++k) better(bv, bi, to_acc(e[k]), i * VEC + k);
     }
     start = nvec * VEC;
   }
-  for (int i = start + threadIdx.x; i < vocab; i += AM_THREADS) better(bv, bi, to_f(row[i]), i);
+  for (int i = start + threadIdx.x; i < vocab; i += AM_THREADS) better(bv, bi, to_acc(row[i]), i);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const A ov = __shfl_xor_sync(0xffffffffu, bv, o);
     const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
     better(bv, bi, ov, oi);
   }
-  __shared__ float sv[AM_THREADS / 32];
+  __shared__ A sv[AM_THREADS / 32];
   __shared__ int si[AM_THREADS / 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
@@ -75,11 +81,17 @@ extern "C" int sd_argmax_rows(const void* logits, int32_t dtype, int64_t row_str
   SD_REQUIRE(vocab >= 1 && rows >= 0, "sd_argmax_rows: bad shape");
   if (rows == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SD_REQUIRE(dtype == SD_DTYPE_F32 || dtype == SD_DTYPE_BF16 || dtype == SD_DTYPE_F64,
+             "sd_argmax_rows: logits must be float32, bfloat16 or float64");
   if (dtype == SD_DTYPE_F32)
-    sd::argmax_kernel<float><<<rows, sd::AM_THREADS, 0, s>>>(static_cast<const float*>(logits), row_stride, vocab, out);
+    sd::argmax_kernel<float, float><<<rows, sd::AM_THREADS, 0, s>>>(static_cast<const float*>(logits), row_stride,
+                                                                    vocab, out);
+  else if (dtype == SD_DTYPE_F64)
+    sd::argmax_kernel<double, double><<<rows, sd::AM_THREADS, 0, s>>>(static_cast<const double*>(logits), row_stride,
+                                                                      vocab, out);
   else
-    sd::argmax_kernel<__nv_bfloat16><<<rows, sd::AM_THREADS, 0, s>>>(static_cast<const __nv_bfloat16*>(logits),
-                                                                      row_stride, vocab, out);
+    sd::argmax_kernel<__nv_bfloat16, float><<<rows, sd::AM_THREADS, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(logits), row_stride, vocab, out);
   sd::count_launch();
   SD_CUDA_RETURN();
 }

@@ -12,7 +12,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) attn_generic_kernel(
     const T* __restrict__ q, T* __restrict__ out, float* __restrict__ lse_out, PagedKv kv,
     int layer, const int32_t* __restrict__ items, const int32_t* __restrict__ crit,
-    float* __restrict__ acc, int64_t acc_stride, const int32_t* __restrict__ planted,
+    unsigned long long* __restrict__ acc, int64_t acc_stride, float acc_scale, const int32_t* __restrict__ planted,
     int n_planted, float bonus, int q_heads, float inv_sqrt_d, float* __restrict__ ws,
     int max_keys, int max_rows) {
   const Item it = load_item(items, blockIdx.y);
@@ -125,8 +125,9 @@ __global__ void __launch_bounds__(256) attn_generic_kernel(
         const float s = S[(int64_t)r * max_keys + j];
         if (s != -INFINITY) sum += expf(((s - sms[r]) + (kbias[j] - smb[r])) - sll[r]);
       }
-      if (sum != 0.f)
-        atomicAdd(acc + (int64_t)(it.acc_row + qt * it.acc_step) * acc_stride + kpos[j], sum);
+      // fixed point (spardec_b200.h): order-independent integer accumulation
+      const unsigned long long u = __float2ull_rn(sum * acc_scale);
+      if (u != 0ull) atomicAdd(acc + (int64_t)(it.acc_row + qt * it.acc_step) * acc_stride + kpos[j], u);
     }
   }
 }
@@ -137,7 +138,8 @@ int64_t generic_ws_bytes(int num_items, int max_keys, int max_rows, int kv_heads
 
 int launch_attn_generic(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer,
                         const int32_t* items, int num_items, int max_keys, int max_nq,
-                        const int32_t* crit, float* acc, int64_t acc_stride, const int32_t* planted,
+                        const int32_t* crit, unsigned long long* acc, int64_t acc_stride, int acc_shift,
+                        const int32_t* planted,
                         int n_planted, float bonus, int q_heads, float scale, void* ws,
                         int64_t ws_bytes, cudaStream_t stream) {
   const int G = q_heads / kvp->kv_heads;
@@ -153,13 +155,13 @@ int launch_attn_generic(const void* q, void* out, float* lse, const sd_paged_kv*
       cudaFuncSetAttribute(attn_generic_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attn_generic_kernel<float><<<grid, 256, smem, stream>>>(
         static_cast<const float*>(q), static_cast<float*>(out), lse, kv, layer, items, crit, acc,
-        acc_stride, planted, n_planted, bonus, q_heads, scale, static_cast<float*>(ws), max_keys, max_rows);
+        acc_stride, ldexpf(1.f, acc_shift), planted, n_planted, bonus, q_heads, scale, static_cast<float*>(ws), max_keys, max_rows);
   } else {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(attn_generic_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attn_generic_kernel<__nv_bfloat16><<<grid, 256, smem, stream>>>(
         static_cast<const __nv_bfloat16*>(q), static_cast<__nv_bfloat16*>(out), lse, kv, layer, items,
-        crit, acc, acc_stride, planted, n_planted, bonus, q_heads, scale, static_cast<float*>(ws),
+        crit, acc, acc_stride, ldexpf(1.f, acc_shift), planted, n_planted, bonus, q_heads, scale, static_cast<float*>(ws),
         max_keys, max_rows);
   }
   count_launch();

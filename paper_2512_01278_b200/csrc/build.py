@@ -20,7 +20,8 @@ PKG = HERE.parent
 ROOT = PKG.parent
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libspardec_b200.so"
-SOURCES = ["abi.cu", "attn_generic.cu", "attn_mma.cu", "rope_kv.cu", "select.cu", "accept.cu", "glue.cu", "attn_ws.cu", "attn_tm.cu", "attn_umma.cu", "forward.cu"]
+SOURCES = ["abi.cu", "attn_generic.cu", "rope_kv.cu", "select.cu", "accept.cu", "glue.cu", "attn_umma.cu",
+           "attn_umma_g4.cu", "attn_umma_g8.cu", "forward.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -29,7 +30,7 @@ FLAGS = [
 ]
 
 
-def _stamp() -> str:
+def source_stamp() -> str:
     h = hashlib.sha256()
     for f in sorted(HERE.glob("*.cu")) + sorted(HERE.glob("*.cuh")) + [ROOT / "include" / "spardec_b200.h"]:
         h.update(f.name.encode())
@@ -40,16 +41,15 @@ def _stamp() -> str:
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     LIB_DIR.mkdir(exist_ok=True)
-    stamp_file = LIB_DIR / "build.stamp"
-    stamp = _stamp()
-    if LIB.exists() and not force and stamp_file.exists() and stamp_file.read_text() == stamp:
+    stamp = source_stamp()
+    if LIB.exists() and not force and _lib_build_id(LIB) == stamp:
         return LIB
     obj_dir = LIB_DIR / "obj"
     obj_dir.mkdir(exist_ok=True)
 
     def compile_one(src: str) -> Path:
         obj = obj_dir / (Path(src).stem + ".o")
-        cmd = [NVCC, *FLAGS, "-c", str(HERE / src), "-o", str(obj)]
+        cmd = [NVCC, *FLAGS, f"-DSD_BUILD_ID=\"{stamp}\"", "-c", str(HERE / src), "-o", str(obj)]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         res = subprocess.run(cmd, capture_output=True, text=True)
@@ -68,8 +68,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
     os.replace(tmp, LIB)
-    stamp_file.write_text(stamp)
     return LIB
+
+
+def _lib_build_id(path: Path) -> str | None:
+    """sd_build_id() of a built library, read in a child process (loading it here would pin
+    the old mapping in this process)."""
+    code = ("import ctypes,sys; l=ctypes.CDLL(sys.argv[1]); l.sd_build_id.restype=ctypes.c_char_p; "
+            "print(l.sd_build_id().decode())")
+    res = subprocess.run([sys.executable, "-c", code, str(path)], capture_output=True, text=True)
+    return res.stdout.strip() if res.returncode == 0 else None
 
 
 if __name__ == "__main__":

@@ -23,17 +23,11 @@ extern "C" int sd_rope_kv_write(const void* qkv, int64_t qkv_row_stride, int32_t
                                 void* q_out, void* stream);
 extern "C" int sd_attention(const void* q, void* out, float* lse, const sd_paged_kv* kv, int32_t layer,
                             const int32_t* items, int32_t num_items, int32_t max_keys, int32_t max_nq,
-                            const int32_t* crit, float* acc, int64_t acc_row_stride, const int32_t* planted,
-                            int32_t num_planted, float planted_bonus, int32_t q_heads, float scale,
-                            void* workspace, int64_t workspace_bytes, int32_t flags, void* stream);
+                            const int32_t* crit, uint64_t* acc, int64_t acc_row_stride, int32_t acc_shift,
+                            const int32_t* planted, int32_t num_planted, float planted_bonus, int32_t q_heads,
+                            float scale, void* workspace, int64_t workspace_bytes, int32_t flags, void* stream);
 
 namespace sd {
-
-int launch_attn_fused(const void* q, void* out, const sd_paged_kv* kvp, int layer, const int32_t* items_v,
-                      int nv_items, int v_max_keys, int v_max_nq, float* acc, int64_t acc_stride,
-                      const int32_t* items_d, int nd_items, int d_max_keys, const int32_t* crit,
-                      const int32_t* planted, int n_planted, float bonus, int q_heads, float scale,
-                      cudaStream_t stream, bool* handled);
 
 __global__ void tanh_bf16_kernel(__nv_bfloat16* x, int64_t n) {
   int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
@@ -106,21 +100,12 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
     if ((rc = sd_rmsnorm_cast(x, rows, hidden, eps, hn, SD_DTYPE_BF16, stream)) != 0) return rc;
     if ((rc = sd::gemm(hd, rows, qkv_w, hidden, hn, w[l].w_qkv, qkv, false, 0.f)) != 0) return rc;
     if ((rc = sd_rope_kv_write(qkv, qkv_w, rows, row_table, row_pos, kv, l, q_heads, q, stream)) != 0) return rc;
-    bool fused = false;
-    if (num_launches == 2 && launches[0].max_nq > 1 && launches[1].max_nq == 1) {  // f3: verify + draft
-      const sd_attn_launch& v = launches[0];
-      const sd_attn_launch& d = launches[1];
-      rc = sd::launch_attn_fused(q, ctx, kv, l, v.items, v.num_items, v.max_keys, v.max_nq, v.acc, v.acc_row_stride,
-                                 d.items, d.num_items, d.max_keys, d.crit, planted, num_planted, planted_bonus,
-                                 q_heads, scale, s, &fused);
-      if (rc != 0) return rc;
-    }
-    for (int i = 0; i < num_launches && !fused; ++i) {
+    for (int i = 0; i < num_launches; ++i) {
       const sd_attn_launch& a = launches[i];
       if (a.num_items == 0) continue;
       if ((rc = sd_attention(q, ctx, nullptr, kv, l, a.items, a.num_items, a.max_keys, a.max_nq, a.crit, a.acc,
-                             a.acc_row_stride, planted, num_planted, planted_bonus, q_heads, scale, workspace,
-                             workspace_bytes, 0, stream)) != 0)
+                             a.acc_row_stride, a.acc_shift, planted, num_planted, planted_bonus, q_heads, scale,
+                             workspace, workspace_bytes, 0, stream)) != 0)
         return rc;
     }
     if ((rc = sd::gemm(hd, rows, hidden, hidden, ctx, w[l].wo, x, true, 1.f)) != 0) return rc;

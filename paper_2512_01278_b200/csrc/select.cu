@@ -1,5 +1,6 @@
 // K3: PillarAttn critical-token selection, one CTA per request.
-//   importance[p] = sum_{t < rows} acc[t][p]          (selection.py:207-218,
+//   importance[p] = 2^-shift sum_{t < rows} acc[t][p]  (selection.py:207-218, fp64 from the
+//                   fixed-point accumulators,
 //                   up to the constant 1/(rows*L*Hq) that cannot change order)
 //   budget        = max(1, min(ceil(s*n - 1e-9), n))   (selection.py:167-183)
 //   positions     = top-budget by value, ties to the lower index, ascending
@@ -121,18 +122,19 @@ __device__ void block_topk(const ValT* vals, int n, int take, int32_t* out) {
 }
 
 __global__ void __launch_bounds__(SEL_THREADS) select_critical_kernel(
-    const float* __restrict__ acc, int64_t acc_req_stride, int64_t acc_row_stride,
+    const unsigned long long* __restrict__ acc, int64_t acc_req_stride, int64_t acc_row_stride, double unit,
     const int32_t* __restrict__ n_rows, const int32_t* __restrict__ kv_len, double sparsity,
-    const int32_t* __restrict__ req_index, float* __restrict__ imp, int64_t imp_stride, int32_t* __restrict__ crit, int64_t crit_stride,
-    int32_t* __restrict__ crit_len, int32_t* __restrict__ budget_out) {
+    const int32_t* __restrict__ req_index, double* __restrict__ imp, int64_t imp_stride, int32_t* __restrict__ crit,
+    int64_t crit_stride, int32_t* __restrict__ crit_len, int32_t* __restrict__ budget_out) {
   const int n = kv_len[blockIdx.x];
   const int rows = n_rows[blockIdx.x];
   const int r = req_index ? req_index[blockIdx.x] : blockIdx.x;
-  float* v = imp + (int64_t)r * imp_stride;
-  const float* a = acc + (int64_t)r * acc_req_stride;
+  double* v = imp + (int64_t)r * imp_stride;
+  const unsigned long long* a = acc + (int64_t)r * acc_req_stride;
+  // fixed-point rows -> fp64, summed in row order (deterministic; the reference sums in fp64)
   for (int p = threadIdx.x; p < n; p += SEL_THREADS) {
-    float s = 0.f;
-    for (int t = 0; t < rows; ++t) s += a[(int64_t)t * acc_row_stride + p];
+    double s = 0.0;
+    for (int t = 0; t < rows; ++t) s += (double)a[(int64_t)t * acc_row_stride + p] * unit;
     v[p] = s;
   }
   __syncthreads();
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_critical_kernel(
     crit_len[r] = take;
     if (budget_out) budget_out[r] = b;
   }
-  block_topk<float, uint32_t>(v, n, take, crit + (int64_t)r * crit_stride);
+  block_topk<double, uint64_t>(v, n, take, crit + (int64_t)r * crit_stride);
 }
 
 template <typename ValT, typename KeyT>
@@ -160,17 +162,19 @@ __global__ void __launch_bounds__(SEL_THREADS) topk_kernel(const ValT* __restric
 
 }  // namespace sd
 
-extern "C" int sd_select_critical(const float* acc, int64_t acc_req_stride, int64_t acc_row_stride,
-                                  const int32_t* n_rows, const int32_t* kv_len, double sparsity,
-                                  int32_t num_requests, const int32_t* req_index, float* importance, int64_t imp_stride, int32_t* crit,
-                                  int64_t crit_stride, int32_t* crit_len, int32_t* budget_out, void* stream) {
+extern "C" int sd_select_critical(const uint64_t* acc, int64_t acc_req_stride, int64_t acc_row_stride,
+                                  int32_t acc_shift, const int32_t* n_rows, const int32_t* kv_len, double sparsity,
+                                  int32_t num_requests, const int32_t* req_index, double* importance,
+                                  int64_t imp_stride, int32_t* crit, int64_t crit_stride, int32_t* crit_len,
+                                  int32_t* budget_out, void* stream) {
   SD_REQUIRE(sparsity > 0.0 && sparsity <= 1.0, "sd_select_critical: sparsity must be in (0, 1]");
   SD_REQUIRE(num_requests >= 0, "sd_select_critical: negative request count");
+  SD_REQUIRE(acc_shift >= 0 && acc_shift <= 62, "sd_select_critical: acc_shift must be in [0, 62]");
   SD_REQUIRE(acc && n_rows && kv_len && importance && crit && crit_len, "sd_select_critical: null pointer");
   if (num_requests == 0) return 0;
   sd::select_critical_kernel<<<num_requests, sd::SEL_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
-      acc, acc_req_stride, acc_row_stride, n_rows, kv_len, sparsity, req_index, importance, imp_stride, crit, crit_stride,
-      crit_len, budget_out);
+      reinterpret_cast<const unsigned long long*>(acc), acc_req_stride, acc_row_stride, ldexp(1.0, -acc_shift), n_rows,
+      kv_len, sparsity, req_index, importance, imp_stride, crit, crit_stride, crit_len, budget_out);
   sd::count_launch();
   SD_CUDA_RETURN();
 }

@@ -55,8 +55,12 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ void red_add(float* p, float v) {
-  asm volatile("red.global.add.f32 [%0], %1;\n" ::"l"(p), "f"(v) : "memory");
+// PillarAttn score accumulation in fixed point: v = round(p * 2^shift) added with an
+// integer reduction, so the sum over heads, CTAs and layers is independent of the
+// order the atomics land in (bitwise reproducible importance; see spardec_b200.h)
+__device__ __forceinline__ void red_add_fx(unsigned long long* p, float v, float scale) {
+  const unsigned long long u = __float2ull_rn(v * scale);
+  if (u != 0ull) asm volatile("red.global.add.u64 [%0], %1;\n" ::"l"(p), "l"(u) : "memory");
 }
 
 // ---- tensor memory / UMMA ----
@@ -83,10 +87,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+// N (a multiple of 8) consecutive fp32 columns, issued back to back; caller waits
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
+  static_assert(N % 8 == 0, "TMEM column group must be a multiple of 8");
+#pragma unroll
+  for (int c = 0; c + 16 <= N; c += 16) tmem_ld16(taddr + c, v + c);
+  if constexpr (N % 16 == 8) tmem_ld8(taddr + N - 8, v + N - 8);
+}
 template <int NR>
 __device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&v)[NR]) {
-#pragma unroll
-  for (int c = 0; c < NR; c += 16) tmem_ld16(taddr + c, v + c);
+  tmem_ld_cols<NR>(taddr, v);
   tmem_wait_ld();
 }
 
@@ -116,7 +136,6 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 
 constexpr int kTraceCtas = 16384;
 constexpr int kTraceSlots = 12;
-static __device__ uint64_t g_trace[kTraceCtas * kTraceSlots];  // per translation unit
 __device__ __forceinline__ uint64_t gtime() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -124,7 +143,7 @@ __device__ __forceinline__ uint64_t gtime() {
 }
 
 struct Params {
-  int trace;  // diagnostics: per-CTA phase timestamps (SD_ATTN_TRACE=1)
+  uint64_t* trace;  // diagnostics: [kTraceCtas][kTraceSlots] per-CTA phase timestamps, or null
   const __nv_bfloat16* q;
   __nv_bfloat16* out;
   float* lse_out;
@@ -132,8 +151,9 @@ struct Params {
   int layer;
   const int32_t* items;
   const int32_t* crit;
-  float* acc;
+  unsigned long long* acc;  // fixed-point score accumulators (2^acc_shift per unit)
   int64_t acc_stride;
+  float acc_scale;           // 2^acc_shift
   const int32_t* planted;
   int n_planted;
   float bonus_log2;
@@ -180,7 +200,7 @@ __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / 
 // ct = key tiles of this launch's chunk.  Gathered (critical-list) items stage a position
 // and a physical slot per key; dense items (dense = 1: no critical list, pages of >= 16
 // tokens) only the chunk's block-table entries, one per page.
-__host__ __device__ inline Layout make_layout(int NR, int NSLOT, int TMAX, int ct, int dense = 0) {
+__host__ __device__ inline Layout make_layout(int NR, int NSLOT, int S, int ct, int dense = 0) {
   Layout L{};
   int o = 0;
   L.ring = o;  o += NSLOT * TILE_BYTES;
@@ -189,7 +209,7 @@ __host__ __device__ inline Layout make_layout(int NR, int NSLOT, int TMAX, int c
   L.pos = o;   o += dense ? (ct * TK / 16 + 2) * 4 : ct * TK * 4;
   L.slot = o;  o += dense ? 0 : ct * TK * 4;
   o = align_up(o, 8);
-  L.bar = o;   o += (2 * NSLOT + 2 * TMAX + 5) * 8;
+  L.bar = o;   o += (2 * NSLOT + 2 * S + 5) * 8;
   L.wm = o;    o += NSW * NR * 4;
   L.wl = o;    o += NSW * NR * 4;
   L.xm = o;    o += 16 * NR * 4;          // [source CTA][row] pushed by every cluster peer
@@ -198,22 +218,6 @@ __host__ __device__ inline Layout make_layout(int NR, int NSLOT, int TMAX, int c
   L.tptr = o;  o += 16;
   L.total = align_up(o, 128) + 1024;  // + slack to 1024-align the dynamic base
   return L;
-}
-
-// Fill order of the producer ring (each fill = one 32 KB K or V tile):
-//   K[0..nt)                    phase 1 (logits -> TMEM, row statistics)
-//   V[nt-TR..nt)                phase 2 over the TR tiles whose logits are still in TMEM
-//   (K[j], V[j]) j < nt-TR      phase 2 over evicted tiles: K re-read, logits recomputed
-// With nt <= TMAX (TR = nt) every K and V row is read exactly once.
-__device__ __forceinline__ void fill_tile(int f, int nt, int TR, int& t, bool& isv) {
-  if (f < nt) {
-    t = f, isv = false;
-  } else if (f < nt + TR) {
-    t = nt - TR + (f - nt), isv = true;
-  } else {
-    const int g = f - nt - TR;
-    t = g >> 1, isv = g & 1;
-  }
 }
 
 }  // namespace umma_attn

@@ -5,6 +5,7 @@ reference's host-side contract checks, before anything is launched."""
 from __future__ import annotations
 
 import ctypes
+import math
 
 import torch
 
@@ -42,14 +43,30 @@ def _zeroed_workspace(nbytes: int, device) -> torch.Tensor:
     return ws
 
 
+def score_shift(rows_per_entry: int, layers: int, q_heads: int) -> int:
+    """Fixed-point scale 2^shift of the score accumulators: the largest possible entry
+    (rows summed into it x layers x q heads, each probability <= 1) stays below 2^62."""
+    worst = max(1, int(rows_per_entry) * int(layers) * int(q_heads))
+    return max(0, min(62, 62 - math.ceil(math.log2(worst))))
+
+
+def scores_to_float(acc: torch.Tensor, shift: int) -> torch.Tensor:
+    """Fixed-point accumulators -> fp64 values (exact up to 2^53 units)."""
+    return acc.double() * (2.0 ** -shift)
+
+
 def attention(q: torch.Tensor, out: torch.Tensor, pool, layer: int, items: torch.Tensor, num_items: int,
               max_keys: int, max_nq: int, q_heads: int, *, crit: torch.Tensor | None = None,
               lse: torch.Tensor | None = None, acc: torch.Tensor | None = None, acc_row_stride: int = 0,
-              planted: torch.Tensor | None = None, planted_bonus: float = 0.0, scale: float | None = None,
-              workspace: torch.Tensor | None = None, force_generic: bool = False) -> None:
-    """K1/K2: paged GQA attention over the work items (see spardec_b200.h)."""
+              acc_shift: int = 0, planted: torch.Tensor | None = None, planted_bonus: float = 0.0,
+              scale: float | None = None, workspace: torch.Tensor | None = None,
+              force_generic: bool = False) -> None:
+    """K1/K2: paged GQA attention over the work items (see spardec_b200.h).  ``acc`` is an
+    int64 tensor of fixed-point score accumulators (unit 2^-acc_shift)."""
     if num_items == 0:
         return
+    if acc is not None and acc.dtype != torch.int64:
+        raise ContractError("attention: score accumulators are int64 fixed point (see score_shift)")
     desc = pool.desc()
     lib = N.lib()
     key = (desc.kv_heads, desc.head_dim, desc.dtype, num_items, max_keys, max_nq, q_heads)
@@ -69,21 +86,23 @@ def attention(q: torch.Tensor, out: torch.Tensor, pool, layer: int, items: torch
     n_planted = 0 if planted is None else planted.numel()
     N.check(lib.sd_attention(q.data_ptr(), out.data_ptr(), N.ptr(lse), ctypes.byref(desc), layer,
                              items.data_ptr(), num_items, max_keys, max_nq, N.ptr(crit), N.ptr(acc),
-                             acc_row_stride, N.ptr(planted), n_planted, planted_bonus, q_heads, scale,
+                             acc_row_stride, acc_shift, N.ptr(planted), n_planted, planted_bonus, q_heads, scale,
                              N.ptr(workspace), ws_bytes, 1 if force_generic else 0, N.stream_handle()),
             "sd_attention")
 
 
-def select_critical(acc: torch.Tensor, acc_req_stride: int, acc_row_stride: int, n_rows: torch.Tensor,
-                    kv_len: torch.Tensor, sparsity: float, num: int, importance: torch.Tensor,
-                    crit: torch.Tensor, crit_len: torch.Tensor, budget: torch.Tensor | None = None,
-                    req_index: torch.Tensor | None = None) -> None:
-    """K3: importance = sum of the surviving score rows; budget; tie-exact top-k.
-    ``req_index[r]`` (optional) redirects request r to row req_index[r] of
+def select_critical(acc: torch.Tensor, acc_req_stride: int, acc_row_stride: int, acc_shift: int,
+                    n_rows: torch.Tensor, kv_len: torch.Tensor, sparsity: float, num: int,
+                    importance: torch.Tensor, crit: torch.Tensor, crit_len: torch.Tensor,
+                    budget: torch.Tensor | None = None, req_index: torch.Tensor | None = None) -> None:
+    """K3: importance (fp64) = sum of the surviving fixed-point score rows; budget; tie-exact
+    top-k.  ``req_index[r]`` (optional) redirects request r to row req_index[r] of
     acc / importance / crit / crit_len / budget."""
     if num == 0:
         return
-    N.check(N.lib().sd_select_critical(acc.data_ptr(), acc_req_stride, acc_row_stride, n_rows.data_ptr(),
+    if acc.dtype != torch.int64 or importance.dtype != torch.float64:
+        raise ContractError("select_critical: int64 accumulators and float64 importance expected")
+    N.check(N.lib().sd_select_critical(acc.data_ptr(), acc_req_stride, acc_row_stride, acc_shift, n_rows.data_ptr(),
                                        kv_len.data_ptr(), float(sparsity), num, N.ptr(req_index),
                                        importance.data_ptr(),
                                        importance.stride(0), crit.data_ptr(), crit.stride(0),

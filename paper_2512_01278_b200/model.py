@@ -30,7 +30,7 @@ from . import _native as N
 from . import kernels as K
 from .errors import ConfigurationError, ContractError
 from .paged import PagedKvPool
-from .selection import AttentionScoreLog, CriticalTokenSet
+from .selection import AttentionScoreLog, CriticalTokenSet, ScoreRow
 
 INIT_SCALE = 0.08   # model.py:31
 RMS_EPS = 1e-6      # model.py:32
@@ -223,8 +223,9 @@ class AttnLaunch:
     max_keys: int
     max_nq: int
     crit: torch.Tensor | None = None
-    acc: torch.Tensor | None = None
+    acc: torch.Tensor | None = None  # int64 fixed-point score accumulators (unit 2^-acc_shift)
     acc_row_stride: int = 0
+    acc_shift: int = 0
     timer: object | None = None   # optional callable(start: bool) for per-launch timing
 
 
@@ -245,7 +246,7 @@ def _side_stream(device) -> torch.cuda.Stream:
 
 def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_table: torch.Tensor,
                  row_pos: torch.Tensor, launches: Sequence[AttnLaunch], lse_out: torch.Tensor | None = None,
-                 force_generic: bool = False) -> torch.Tensor:
+                 force_generic: bool = False, q_trace: list | None = None) -> torch.Tensor:
     """Run every layer for R rows at once and return the final hidden (R, h) fp32.
 
     Row r is token ``tokens[r]`` at absolute position ``row_pos[r]`` of the
@@ -261,7 +262,7 @@ def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_t
     Hq, d = c.num_q_heads, c.head_dim
     dt = model.dtype
     x = model.embedding.index_select(0, tokens.long()).float()
-    if (NATIVE_FORWARD and dt == torch.bfloat16 and lse_out is None and not force_generic
+    if (NATIVE_FORWARD and dt == torch.bfloat16 and lse_out is None and not force_generic and q_trace is None
             and all(ln.timer is None for ln in launches)):
         return _forward_native(model, pool, tokens, row_table, row_pos, launches, x)
     hn = torch.empty(R, c.hidden_dim, dtype=dt, device=model.device)
@@ -278,7 +279,7 @@ def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_t
             ln.timer(True)
         K.attention(q_buf, ctx, pool, l, ln.items, ln.num_items, ln.max_keys, ln.max_nq, Hq,
                     crit=ln.crit, lse=None if lse_out is None else lse_out[l], acc=ln.acc,
-                    acc_row_stride=ln.acc_row_stride, planted=model.planted_dev,
+                    acc_row_stride=ln.acc_row_stride, acc_shift=ln.acc_shift, planted=model.planted_dev,
                     planted_bonus=model.planted_bonus, force_generic=force_generic)
         if ln.timer is not None:
             ln.timer(False)
@@ -287,6 +288,8 @@ def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_t
         K.rmsnorm_cast(x, hn, RMS_EPS)
         qkv = torch.mm(hn, model.w_qkv[l])
         K.rope_kv_write(qkv, row_table, row_pos, pool, l, Hq, q_buf)
+        if q_trace is not None:
+            q_trace.append(q_buf.clone())
         if side is None:
             for ln in launches:
                 attend(ln, l)
@@ -310,6 +313,9 @@ def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_t
 
 
 NATIVE_FORWARD = True  # bf16: the layer loop runs in the library (sd_forward_layers), one host call
+# query rows (tokens x GQA group) per attention work item for multi-token windows (prefill,
+# forward_full): <= 48 keeps the tcgen05 verify kernel at two CTAs per SM
+ITEM_ROWS = 48
 
 
 def _forward_native(model: ToyModel, pool: PagedKvPool, tokens, row_table, row_pos, launches, x):
@@ -340,6 +346,7 @@ def _forward_native(model: ToyModel, pool: PagedKvPool, tokens, row_table, row_p
         descs[i].crit = N.ptr(ln.crit)
         descs[i].acc = N.ptr(ln.acc)
         descs[i].acc_row_stride = ln.acc_row_stride
+        descs[i].acc_shift = ln.acc_shift
         need = max(need, lib.sd_attention_workspace_bytes(ln.num_items, ln.max_keys, ln.max_nq, Hq,
                                                           ctypes.byref(desc)))
     ws = K._zeroed_workspace(need, dev) if need > 0 else None
@@ -492,19 +499,59 @@ def forward_full(model: ToyModel, committed_kv: KvCache, new_tokens: Sequence[in
     committed_kv.ensure_capacity(n0 + n)
     pool = committed_kv.pool
     dev = model.device
-    acc = torch.zeros(n, n0 + n, dtype=torch.float32, device=dev) if capture_scores else None
+    shift = K.score_shift(1, cfg.num_layers, cfg.num_q_heads)
+    acc = torch.zeros(n, n0 + n, dtype=torch.int64, device=dev) if capture_scores else None
     lse = torch.empty(cfg.num_layers, n, cfg.num_q_heads, dtype=torch.float32, device=dev) if capture_scores else None
-    items = make_items([(0, 0, n, n0, 0, 0, 0, 0 if capture_scores else -1, 1)], dev)
-    launch = AttnLaunch(items, 1, n0 + n, n, acc=acc, acc_row_stride=n0 + n)
+    # one work item per window of ITEM_ROWS query rows (token j attends causally to [0, n0+j]):
+    # every chunk is a tcgen05 verify tile on the bf16 production shapes
+    step = max(1, ITEM_ROWS // cfg.group_size)
+    rows = [(0, q0, min(step, n - q0), n0 + q0, 0, 0, 0, q0 if capture_scores else -1, 1)
+            for q0 in range(0, n, step)]
+    items = make_items(rows, dev)
+    launch = AttnLaunch(items, len(rows), n0 + n, min(step, n), acc=acc, acc_row_stride=n0 + n, acc_shift=shift)
     tok = torch.tensor(toks, dtype=torch.int32, device=dev)
     rt = torch.zeros(n, dtype=torch.int32, device=dev)
     rp = torch.arange(n0, n0 + n, dtype=torch.int32, device=dev)
-    x = forward_rows(model, pool, tok, rt, rp, [launch], lse_out=lse)
+    q_trace = [] if capture_scores else None
+    x = forward_rows(model, pool, tok, rt, rp, [launch], lse_out=lse, q_trace=q_trace)
     logits = lm_head(model, x)
     ks, vs = pool.read(0, range(n0, n0 + n))
     entries = [KVEntry(k=ks[j].clone(), v=vs[j].clone()) for j in range(n)]
-    log = AttentionScoreLog(cfg.num_q_heads, cfg.num_kv_heads, cfg.num_layers, n0, acc, lse)
+    rows_fn = _score_rows_fn(model, pool, n0, n, q_trace, lse) if capture_scores else None
+    log = AttentionScoreLog.from_accumulators(cfg.num_q_heads, cfg.num_kv_heads, cfg.num_layers, n0, acc, lse,
+                                              acc_shift=shift, rows_fn=rows_fn,
+                                              dtype_tol=1e-4 if model.dtype == torch.float32 else 2e-2)
     return logits, entries, log
+
+
+def _score_rows_fn(model: ToyModel, pool: PagedKvPool, n0: int, n: int, q_trace: list, lse: torch.Tensor):
+    """Deferred ScoreRow materialisation for AttentionScoreLog.layers (debug / API parity
+    only): logits = q . k / sqrt(d) (+ planted bonus) in fp64 from the captured rotated
+    queries and the cache's keys, rows causal as in model.py:318-334."""
+    c = model.config
+
+    def rows():
+        ks, _ = pool.read(0, range(n0 + n))            # (n0 + n, L, Hkv, d)
+        kd = ks.double()
+        bonus = torch.zeros(n0 + n, dtype=torch.float64, device=kd.device)
+        if model.planted is not None:
+            pp = [p for p in model.planted.positions if p < n0 + n]
+            if pp:
+                bonus[torch.tensor(pp, device=kd.device)] = model.planted_bonus
+        scale = 1.0 / math.sqrt(c.head_dim)
+        out = []
+        for l in range(c.num_layers):
+            kl = kd[:, l].repeat_interleave(c.group_size, dim=1)   # (n0 + n, Hq, d)
+            ql = q_trace[l].double()                             # (n, Hq, d)
+            layer_rows = []
+            for q in range(n):
+                w = n0 + q + 1
+                lg = torch.einsum("hd,jhd->hj", ql[q], kl[:w]) * scale + bonus[:w]
+                layer_rows.append(ScoreRow(logits=lg, lse=lse[l, q].double()))
+            out.append(layer_rows)
+        return out
+
+    return rows
 
 
 def forward_sparse(model: ToyModel, committed_kv: KvCache, critical: CriticalTokenSet,
@@ -537,12 +584,13 @@ def forward_sparse(model: ToyModel, committed_kv: KvCache, critical: CriticalTok
 
 
 def greedy_token(logits) -> int:
-    """Argmax with ties to the lowest token id (model.py:388-390), on device."""
+    """Argmax with ties to the lowest token id (model.py:388-390), on device; fp64 rows
+    (the reference's dtype) are compared in fp64."""
     t = logits if isinstance(logits, torch.Tensor) else torch.as_tensor(np.asarray(logits))
     if not t.is_cuda:
         t = t.cuda()
-    if t.dtype not in (torch.float32, torch.bfloat16):
-        t = t.float()
+    if t.dtype not in (torch.float32, torch.bfloat16, torch.float64):
+        t = t.double()
     t = t.reshape(1, -1).contiguous()
     out = torch.empty(1, dtype=torch.int32, device=t.device)
     K.argmax_rows(t, out)

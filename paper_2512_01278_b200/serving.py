@@ -30,9 +30,9 @@ from .model import AttnLaunch, ToyModel, forward_rows, lm_head
 from .paged import PagedKvPool
 from .selection import compute_budget
 
-# rows per prefill work item (query tokens x GQA group): <= 64 keeps prefill on the tcgen05
-# kernel (128 x 4608-token prefill: 9.4 s; 80 rows on the mma.sync fallback: 163 s)
-MMA_MAX_ROWS = int(os.environ.get("SD_PREFILL_ROWS", "64"))
+# rows per prefill work item (query tokens x GQA group); the tcgen05 verify kernel takes up to
+# 80 rows, two CTAs per SM up to 48
+MMA_MAX_ROWS = int(os.environ.get("SD_PREFILL_ROWS", "48"))
 
 
 @dataclass
@@ -89,8 +89,11 @@ class BatchedDecoder:
         self.crit = torch.zeros(max_requests, self.crit_cap, dtype=torch.int32, device=self.dev)
         self.crit_len_dev = torch.zeros(max_requests, dtype=torch.int32, device=self.dev)
         self.acc_w = self.max_seq_len
-        self.acc = torch.zeros(max_requests * (k + 1), self.acc_w, dtype=torch.float32, device=self.dev)
-        self.imp = torch.zeros(max_requests, self.acc_w, dtype=torch.float32, device=self.dev)
+        # fixed-point score accumulators (kernels.score_shift): one row per verify query token
+        self.acc = torch.zeros(max_requests * (k + 1), self.acc_w, dtype=torch.int64, device=self.dev)
+        self.imp = torch.zeros(max_requests, self.acc_w, dtype=torch.float64, device=self.dev)
+        self.verify_shift = K.score_shift(1, c.num_layers, c.num_q_heads)
+        self.prefill_shift = K.score_shift(self.max_seq_len, c.num_layers, c.num_q_heads)  # prompt rows sum
         self.free_slots = list(range(max_requests - 1, -1, -1))
         self.seqs: dict = {}
         self._host_kv: dict = {}     # request -> {position: (K rows, V rows)} pinned host copies
@@ -237,7 +240,7 @@ class BatchedDecoder:
             s.n_kv = len(pr)
             if not s.done:
                 refresh.append((s, 1))
-        self._refresh(refresh)
+        self._refresh(refresh, self.prefill_shift)
         return seqs
 
     def _prefill_group(self, seqs) -> None:
@@ -257,10 +260,11 @@ class BatchedDecoder:
                 items.append((s.slot, row + q0, nq, q0, 0, 0, 0, acc_row, 0))
             row += P
         max_p = max(len(s.prompt) for s in seqs)
-        self.acc.view(self.max_requests, self.k + 1, self.acc_w)[[s.slot for s in seqs], 0] = 0.0
+        self.acc.view(self.max_requests, self.k + 1, self.acc_w)[[s.slot for s in seqs], 0] = 0
+        shift = self.prefill_shift  # all prompt rows sum into one accumulator row
         tok = torch.tensor(toks, dtype=torch.int32, device=self.dev)
         launch = AttnLaunch(_items(items, self.dev), len(items), max_p, min(chunk, max_p), acc=self.acc,
-                            acc_row_stride=self.acc_w)
+                            acc_row_stride=self.acc_w, acc_shift=shift)
         x = forward_rows(self.model, self.pool, tok, _i32(rt, self.dev), _i32(rp, self.dev), [launch])
         last = torch.tensor(np.cumsum([len(s.prompt) for s in seqs]) - 1, device=self.dev)
         first = _argmax(lm_head(self.model, x.index_select(0, last))).cpu().tolist()
@@ -272,16 +276,16 @@ class BatchedDecoder:
             s.stats.emitted_tokens = len(s.committed)
             if not s.done:
                 refresh.append((s, 1))
-        self._refresh(refresh)
+        self._refresh(refresh, shift)
 
-    def _refresh(self, pairs) -> None:
+    def _refresh(self, pairs, shift: int) -> None:
         """K3 for (seq, surviving rows) pairs: importance -> budget -> top-k."""
         if not pairs:
             return
         slots = [s.slot for s, _ in pairs]
         n_rows = [n for _, n in pairs]
         kv = [s.n_kv for s, _ in pairs]
-        K.select_critical(self.acc, (self.k + 1) * self.acc.stride(0), self.acc.stride(0), _i32(n_rows, self.dev),
+        K.select_critical(self.acc, (self.k + 1) * self.acc.stride(0), self.acc.stride(0), shift, _i32(n_rows, self.dev),
                           _i32(kv, self.dev), self.sparsity, len(pairs), self.imp, self.crit, self.crit_len_dev,
                           req_index=_i32(slots, self.dev))
         for s, _ in pairs:
@@ -334,9 +338,10 @@ class BatchedDecoder:
         launches = []
         if v_items:
             slots = torch.tensor([s.slot for s in verifs], device=self.dev)
-            self.acc.view(self.max_requests, self.k + 1, self.acc_w)[slots] = 0.0
+            self.acc.view(self.max_requests, self.k + 1, self.acc_w)[slots] = 0
             launches.append(AttnLaunch(_items(v_items, self.dev), len(v_items), v_max_keys, v_max_nq, acc=self.acc,
-                                       acc_row_stride=self.acc_w, timer=self._timer("verify")))
+                                       acc_row_stride=self.acc_w, acc_shift=self.verify_shift,
+                                       timer=self._timer("verify")))
         if d_items:  # after the verify launch: it runs on the side stream (model.forward_rows)
             launches.append(AttnLaunch(_items(d_items, self.dev), len(d_items), d_max_keys, 1, crit=self.crit,
                                        timer=self._timer("draft")))
@@ -377,7 +382,7 @@ class BatchedDecoder:
             accepted[s.request_id] = a
             if not s.done:
                 refresh.append((s, a + 1))
-        self._refresh(refresh)
+        self._refresh(refresh, self.verify_shift)
         self.last_rows = R
         return StepResult(accepted, emitted, R, n_draft_rows, R - n_draft_rows)
 

@@ -144,10 +144,13 @@ class _Live:
 
 def run_token_sim(workload: WorkloadSpec, model_config: ModelConfig, cfg: SimConfig, kv_cfg: KvPoolConfig,
                   params=None, *, model: ToyModel | None = None, dtype: torch.dtype = torch.float32,
-                  check_lossless: bool = False) -> SimReport:
+                  check_lossless: bool = True) -> SimReport:
     """Serve ``workload`` with the real model on the GPU; returns the same
     report fields as the reference.  ``params`` (cost model) is accepted for
-    signature parity and ignored: latency is measured."""
+    signature parity and ignored: latency is measured.  Like the reference
+    (simulate.py:245-248), every completed request is checked against the
+    autoregressive oracle (greedy_decode on the same model) unless
+    ``check_lossless=False``."""
     if model is None:
         model = init_model(model_config, dtype=dtype)
     if kv_cfg.policy is KvPolicy.PREEMPT:
@@ -264,6 +267,10 @@ def run_token_sim(workload: WorkloadSpec, model_config: ModelConfig, cfg: SimCon
             else:
                 pressure_now = True
                 lives[rid].pressure_absences += 1
+        if not ex_d and not ex_v and not to_prefill and not stalled_now and not pressure_now \
+                and not pool.transfers_pending and lives and not waiting:
+            # deadlock guard (simulate.py:462-463): nothing runnable and nothing in flight
+            raise SimulationError("no schedulable work and no pending transfers")
         result = dec.step(ex_d, ex_v)
         torch.cuda.synchronize()
         latency = (time.perf_counter() - t0) * 1000.0

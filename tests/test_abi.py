@@ -27,7 +27,8 @@ def test_library_loads_and_exports_every_symbol():
     for name in _declared():
         assert hasattr(lib, name), name
     assert set(_declared()) == set(N.SIGNATURES)
-    assert lib.sd_abi_version() == 1
+    assert lib.sd_abi_version() == N.ABI_VERSION == 2
+    assert lib.sd_build_id().decode() == N.source_build_id()  # built from these sources
     assert lib.sd_last_error() == b""
 
 
@@ -36,7 +37,7 @@ def test_contract_violation_maps_to_contract_error():
     from paper_2512_01278_b200 import _native as N
     from paper_2512_01278_b200.errors import ContractError
     lib = N.load_library()
-    rc = lib.sd_select_critical(None, 0, 0, None, None, 0.5, 1, None, None, 0, None, 0, None, None, None)
+    rc = lib.sd_select_critical(None, 0, 0, 0, None, None, 0.5, 1, None, None, 0, None, 0, None, None, None)
     assert rc < 0
     with pytest.raises(ContractError, match="null pointer"):
         N.check(rc, "sd_select_critical")

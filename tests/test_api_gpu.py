@@ -65,15 +65,12 @@ def test_forwards_match_reference(golden_forwards, tag, shp, planted):
     for a in (0, 2, 4):
         imp = S.importance_from_log(log2.slice_queries(a + 1), n_kv + a + 1).double().cpu().numpy()
         np.testing.assert_allclose(imp, g[f"importance_a{a}"], rtol=1e-4, atol=1e-6)
-    imp_p = S.importance_from_log(log, n_kv)
     crit = S.select_from_log(log, n_kv, 0.1)
-    # bit-exact given identical scores: our K3 on our fp32 accumulator vs the stable sort
-    acc_sum = log.acc[: log.num_queries(), :n_kv].sum(dim=0)
+    # bit-exact given identical scores: our K3 on our fixed-point accumulators vs the stable sort
     assert crit.positions.tolist() == O.topk_ascending(
         _k3_importance(log, n_kv), O.budget_for(n_kv, 0.1)).tolist()
     # and the reference's own (fp64) choice on these configs
     assert crit.positions.tolist() == g["prefill_critical"].tolist()
-    del imp_p, acc_sum
     l1, e1 = M.forward_sparse(model, cache, crit, [], toks[-5])
     np.testing.assert_allclose(l1.double().cpu().numpy(), g["sparse_logits1"], atol=1e-4)
     np.testing.assert_allclose(e1.k.double().cpu().numpy(), g["sparse_k1"], atol=1e-4)
@@ -82,12 +79,12 @@ def test_forwards_match_reference(golden_forwards, tag, shp, planted):
 
 
 def _k3_importance(log, n_kv):
-    """The exact fp32 values K3 sums (rows ascending), as float64."""
+    """The exact fp64 values K3 forms (fixed-point rows -> fp64, rows ascending)."""
     acc = log.acc.cpu().numpy()
-    v = np.zeros(n_kv, dtype=np.float32)
+    v = np.zeros(n_kv, dtype=np.float64)
     for t in range(log.num_queries()):
-        v = (v + acc[t, :n_kv]).astype(np.float32)
-    return v.astype(np.float64)
+        v = v + acc[t, :n_kv].astype(np.float64) * 2.0 ** -log.acc_shift
+    return v
 
 
 def _run_stream_case(c):
@@ -178,9 +175,9 @@ def test_native_layer_loop_matches_python_loop_bf16(planted):
         rp = torch.tensor([n0 + i for i in range(5)] + [n0 + 2], dtype=torch.int32, device=dev)
         crit = torch.tensor(sorted(rng.choice(n0, 20, replace=False).tolist()) if not results else results[0][4],
                             dtype=torch.int32, device=dev)
-        acc = torch.zeros(5, n0 + 8, dtype=torch.float32, device=dev)
+        acc = torch.zeros(5, n0 + 8, dtype=torch.int64, device=dev)
         launches = [AttnLaunch(make_items([(0, 0, 5, n0, 0, 0, 0, 0, 1)], dev), 1, n0 + 5, 5, acc=acc,
-                               acc_row_stride=n0 + 8),
+                               acc_row_stride=n0 + 8, acc_shift=40),
                     AttnLaunch(make_items([(1, 5, 1, n0 + 2, 0, 20, n0, -1, 0)], dev), 1, 23, 1, crit=crit)]
         old = M.NATIVE_FORWARD
         M.NATIVE_FORWARD = native
@@ -191,7 +188,7 @@ def test_native_layer_loop_matches_python_loop_bf16(planted):
         logits = lm_head(model, x)
         torch.cuda.synchronize()
         kk, _ = pool.read(0, range(n0, n0 + 5))
-        results.append((logits.float().cpu(), acc.cpu(), kk.float().cpu(), toks, crit.tolist()))
+        results.append((logits.float().cpu(), acc.double().cpu() * 2.0 ** -40, kk.float().cpu(), toks, crit.tolist()))
     (ln, an, kn, _, _), (lp, ap, kp, _, _) = results
     scale = lp.abs().max().item()
     assert (ln - lp).abs().max().item() <= 2e-2 * max(1.0, scale)

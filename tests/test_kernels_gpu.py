@@ -26,6 +26,15 @@ from paper_2512_01278_b200.paged import PagedKvPool  # noqa: E402
 DEV = torch.device("cuda")
 
 
+def _acc(rows, width, Hq, L=1):
+    """Zeroed fixed-point score accumulators and their shift (one row per query token)."""
+    return torch.zeros(rows, width, dtype=torch.int64, device=DEV), K.score_shift(1, L, Hq)
+
+
+def _accf(acc, shift):
+    return K.scores_to_float(acc, shift).cpu().numpy()
+
+
 def _pool(L, Hkv, d, n_tokens, rows, dtype, page=16, shuffle_seed=None):
     pages_per_row = -(-n_tokens // page)
     pool = PagedKvPool(L, Hkv, d, pages_per_row * rows + 3, page, rows, pages_per_row, dtype, DEV)
@@ -81,12 +90,13 @@ def test_verify_attention_matches_oracle(dtype, force_generic, d, G):
     q = torch.from_numpy(rng.normal(size=(nq, Hq, d))).to(DEV, dtype)
     out = torch.empty_like(q)
     lse = torch.empty(nq, Hq, dtype=torch.float32, device=DEV)
-    acc = torch.zeros(nq, n0 + nq, dtype=torch.float32, device=DEV)
+    acc, shift = _acc(nq, n0 + nq, Hq)
     items = make_items([(1, 0, nq, n0, 0, 0, 0, 0, 1)], DEV)
     planted = torch.tensor([3, 77, 400], dtype=torch.int32, device=DEV)
     for use_planted in (False, True):
         acc.zero_()
         K.attention(q, out, pool, 1, items, 1, n0 + nq, nq, Hq, lse=lse, acc=acc, acc_row_stride=n0 + nq,
+                    acc_shift=shift,
                     planted=planted if use_planted else None, planted_bonus=3.0 if use_planted else 0.0,
                     force_generic=force_generic)
         torch.cuda.synchronize()
@@ -95,7 +105,7 @@ def test_verify_attention_matches_oracle(dtype, force_generic, d, G):
         tol = 1e-4 if dtype == torch.float32 else 2e-2
         assert np.abs(out.double().cpu().numpy() - ro).max() <= tol
         assert np.abs(lse.double().cpu().numpy() - rl).max() <= (1e-4 if dtype == torch.float32 else 2e-2)
-        acc_h = acc.double().cpu().numpy()
+        acc_h = _accf(acc, shift)
         for t in range(nq):
             want = np.zeros(n0 + nq)
             for p_, val in ra[t].items():
@@ -182,8 +192,9 @@ def test_batched_items_mixed_lengths_bf16():
     out = torch.empty_like(q)
     lse = torch.empty(len(lens) * nq, Hq, dtype=torch.float32, device=DEV)
     W = max(lens) + nq
-    acc = torch.zeros(len(lens) * nq, W, dtype=torch.float32, device=DEV)
-    K.attention(q, out, pool, 0, items, len(lens), max(lens) + nq, nq, Hq, lse=lse, acc=acc, acc_row_stride=W)
+    acc, shift = _acc(len(lens) * nq, W, Hq)
+    K.attention(q, out, pool, 0, items, len(lens), max(lens) + nq, nq, Hq, lse=lse, acc=acc, acc_row_stride=W,
+                acc_shift=shift)
     torch.cuda.synchronize()
     for r, n in enumerate(lens):
         kr, vr = pool.read(r, range(n + nq))
@@ -192,7 +203,7 @@ def test_batched_items_mixed_lengths_bf16():
         ro, rl, ra = _ref_rows(qs, kr, vr, Hq, Hkv, d, [], range(n + nq), n)
         assert np.abs(out[r * nq:(r + 1) * nq].double().cpu().numpy() - ro).max() <= 2e-2
         assert np.abs(lse[r * nq:(r + 1) * nq].double().cpu().numpy() - rl).max() <= 2e-2
-        a = acc[r * nq:(r + 1) * nq].double().cpu().numpy()
+        a = _accf(acc[r * nq:(r + 1) * nq], shift)
         # each query's probabilities sum to 1 per q head: Hq in total
         np.testing.assert_allclose(a.sum(axis=1), Hq * np.ones(nq), rtol=2e-2)
         for t in range(nq):
@@ -217,14 +228,14 @@ def test_verify_attention_long_context_bf16(n0, G, nq):
     out = torch.empty_like(q)
     lse = torch.empty(nq, Hq, dtype=torch.float32, device=DEV)
     W = n0 + nq
-    acc = torch.zeros(nq, W, dtype=torch.float32, device=DEV)
+    acc, shift = _acc(nq, W, Hq)
     items = make_items([(0, 0, nq, n0, 0, 0, 0, 0, 1)], DEV)
-    K.attention(q, out, pool, 0, items, 1, n0 + nq, nq, Hq, lse=lse, acc=acc, acc_row_stride=W)
+    K.attention(q, out, pool, 0, items, 1, n0 + nq, nq, Hq, lse=lse, acc=acc, acc_row_stride=W, acc_shift=shift)
     torch.cuda.synchronize()
     ro, rl, ra = _ref_rows(q.double().cpu().numpy(), kr, vr, Hq, Hkv, d, [], range(n0 + nq), n0)
     assert np.abs(out.double().cpu().numpy() - ro).max() <= 2e-2
     assert np.abs(lse.double().cpu().numpy() - rl).max() <= 2e-2
-    a = acc.double().cpu().numpy()
+    a = _accf(acc, shift)
     np.testing.assert_allclose(a.sum(axis=1), Hq * np.ones(nq), rtol=2e-2)
     for t in range(nq):
         want = np.zeros(W)
@@ -274,9 +285,10 @@ def test_verify_mixed_token_counts_short_contexts_bf16():
     q = torch.from_numpy(rng.normal(size=(q0, Hq, d))).to(DEV, torch.bfloat16)
     out = torch.empty_like(q)
     lse = torch.empty(q0, Hq, dtype=torch.float32, device=DEV)
-    acc = torch.zeros(len(cases) * 5, maxn, dtype=torch.float32, device=DEV)
+    acc, shift = _acc(len(cases) * 5, maxn, Hq)
     planted = (5, 128, 1001)
     K.attention(q, out, pool, 0, items, len(cases), maxn, 5, Hq, lse=lse, acc=acc, acc_row_stride=maxn,
+                acc_shift=shift,
                 planted=torch.tensor(planted, dtype=torch.int32, device=DEV), planted_bonus=1.5)
     torch.cuda.synchronize()
     q0 = 0
@@ -287,14 +299,14 @@ def test_verify_mixed_token_counts_short_contexts_bf16():
         ro, rl, ra = _ref_rows(qs, kr, vr, Hq, Hkv, d, [], range(n + t), n, planted=planted, bonus=1.5)
         assert np.abs(out[q0:q0 + t].double().cpu().numpy() - ro).max() <= 2e-2
         assert np.abs(lse[q0:q0 + t].double().cpu().numpy() - rl).max() <= 2e-2
-        a = acc[r * 5:r * 5 + t].double().cpu().numpy()
+        a = _accf(acc[r * 5:r * 5 + t], shift)
         for tk in range(t):
             want = np.zeros(maxn)
             for p_, val in ra[tk].items():
                 want[p_] = val
             assert np.abs(a[tk] - want).max() <= 2e-2
         if t < 5:
-            assert acc[r * 5 + t:r * 5 + 5].abs().max().item() == 0.0  # rows of absent tokens untouched
+            assert acc[r * 5 + t:r * 5 + 5].abs().max().item() == 0  # rows of absent tokens untouched
         q0 += t
 
 
@@ -334,56 +346,63 @@ def test_topk_random_float32_vs_stable_sort():
 def test_select_critical_budget_and_rows(golden_budgets):
     rng = np.random.default_rng(3)
     B, rows, W = 6, 5, 9000
-    acc = torch.from_numpy(rng.random((B, rows, W)).astype(np.float32)).to(DEV)
-    acc[2] = 0.0  # all ties
+    shift = 40
+    acc_h = rng.integers(0, 1 << 40, size=(B, rows, W), dtype=np.int64)
+    acc_h[2] = 0  # all ties
+    acc_h[4] = (acc_h[4] >> 36) << 36  # coarse values: many ties
+    acc = torch.from_numpy(acc_h).to(DEV)
     kv_len = np.array([0, 1, 4000, 8999, 1000, 560], dtype=np.int32)
     n_rows = np.array([1, 2, 3, 5, 4, 1], dtype=np.int32)
     for s in (0.05, 0.07, 0.01, 1.0):
-        imp = torch.zeros(B, W, dtype=torch.float32, device=DEV)
+        imp = torch.zeros(B, W, dtype=torch.float64, device=DEV)
         crit = torch.zeros(B, W, dtype=torch.int32, device=DEV)
         clen = torch.zeros(B, dtype=torch.int32, device=DEV)
         bud = torch.zeros(B, dtype=torch.int32, device=DEV)
-        K.select_critical(acc, acc.stride(0), acc.stride(1), torch.from_numpy(n_rows).to(DEV),
+        K.select_critical(acc, acc.stride(0), acc.stride(1), shift, torch.from_numpy(n_rows).to(DEV),
                           torch.from_numpy(kv_len).to(DEV), s, B, imp, crit, clen, bud)
         torch.cuda.synchronize()
         for r in range(B):
             n = int(kv_len[r])
-            want_imp = acc[r, : n_rows[r], :n].double().cpu().numpy()
             got_imp = imp[r, :n].cpu().numpy()
-            # summation order is fixed (rows ascending, fp32)
-            ref32 = np.zeros(n, dtype=np.float32)
-            for t in range(n_rows[r]):
-                ref32 = (ref32 + acc[r, t, :n].cpu().numpy()).astype(np.float32)
-            assert np.array_equal(got_imp, ref32)
+            # fixed point -> fp64, rows ascending: exact (every partial sum < 2^53 units)
+            want_imp = acc_h[r, : n_rows[r], :n].astype(np.float64).sum(axis=0) * 2.0 ** -shift
+            assert np.array_equal(got_imp, want_imp)
             b = O.budget_for(n, s)
             assert int(bud[r]) == b
-            want = O.topk_ascending(got_imp.astype(np.float64), b) if n else np.zeros(0, dtype=np.int64)
+            want = O.topk_ascending(want_imp, b) if n else np.zeros(0, dtype=np.int64)
             assert int(clen[r]) == min(b, n)
             assert crit[r, : min(b, n)].cpu().tolist() == want.tolist()
-            del want_imp
     # device budget formula == reference on every golden (n, s)
     for n, s, b in golden_budgets:
         if n > W:
             continue
         clen = torch.zeros(1, dtype=torch.int32, device=DEV)
         bud = torch.zeros(1, dtype=torch.int32, device=DEV)
-        K.select_critical(acc, 0, acc.stride(1), torch.tensor([1], dtype=torch.int32, device=DEV),
+        K.select_critical(acc, 0, acc.stride(1), shift, torch.tensor([1], dtype=torch.int32, device=DEV),
                           torch.tensor([n], dtype=torch.int32, device=DEV), s, 1,
-                          torch.zeros(1, W, device=DEV), torch.zeros(1, W, dtype=torch.int32, device=DEV), clen, bud)
+                          torch.zeros(1, W, dtype=torch.float64, device=DEV),
+                          torch.zeros(1, W, dtype=torch.int32, device=DEV), clen, bud)
         assert int(bud.item()) == b, (n, s)
 
 
 def test_argmax_and_accept():
     rng = np.random.default_rng(4)
-    for dt in (torch.float32, torch.bfloat16):
+    for dt in (torch.float32, torch.bfloat16, torch.float64):
         logits = rng.normal(size=(37, 151936)).astype(np.float32)
         logits[3, [5, 9, 100]] = 50.0  # tie -> lowest id
         logits[4, :] = 1.0
         t = torch.from_numpy(logits).to(DEV, dt)
         out = torch.empty(37, dtype=torch.int32, device=DEV)
         K.argmax_rows(t, out)
-        want = np.argmax(t.float().cpu().numpy(), axis=1)
+        want = np.argmax(t.double().cpu().numpy(), axis=1)
         assert out.cpu().numpy().tolist() == want.tolist()
+    # fp64 rows whose top two differ below fp32 resolution: compared in fp64 (model.py:388-390)
+    r64 = torch.zeros(2, 1000, dtype=torch.float64, device=DEV)
+    r64[0, 10], r64[0, 900] = 1.0, 1.0 + 1e-12
+    r64[1, 20], r64[1, 7] = 3.0, 3.0 - 1e-13
+    out = torch.empty(2, dtype=torch.int32, device=DEV)
+    K.argmax_rows(r64, out)
+    assert out.cpu().tolist() == [900, 20]
     # accept rule (engine.py:231-239)
     targets = torch.tensor([5, 6, 7, 8, 9, 1, 2, 3, 4], dtype=torch.int32, device=DEV)
     tokens = torch.tensor([0, 5, 6, 0, 9, 0, 2, 9, 4], dtype=torch.int32, device=DEV)
@@ -415,3 +434,143 @@ def test_rope_kv_write_matches_oracle():
         assert np.abs(q_out[r].double().cpu().numpy() - want_q).max() < 1e-5
         assert np.abs(kk[0, 1].double().cpu().numpy() - want_k).max() < 1e-5
         assert np.array_equal(vv[0, 1].double().cpu().numpy(), want_v.astype(np.float32).astype(np.float64))
+
+
+def _verify_case(n0s, nq, G, Hkv=8, seed=0, shuffle=5, scale=1.0, planted=()):
+    """One launch of len(n0s) verify items (nq tokens each) vs the oracle: outputs, lse and
+    per-token fixed-point scores (model.py:229-253, selection.py:78-135)."""
+    rng = np.random.default_rng(seed)
+    d, Hq = 128, Hkv * G
+    B = len(n0s)
+    maxn = max(n0s) + nq
+    pool = _pool(1, Hkv, d, maxn, B, torch.bfloat16, shuffle_seed=shuffle)
+    for r, n in enumerate(n0s):
+        _fill(pool, r, n + nq, rng, scale=scale)
+    items = make_items([(r, r * nq, nq, n, 0, 0, 0, r * nq, 1) for r, n in enumerate(n0s)], DEV)
+    q = torch.from_numpy(rng.normal(size=(B * nq, Hq, d))).to(DEV, torch.bfloat16)
+    out = torch.empty_like(q)
+    lse = torch.empty(B * nq, Hq, dtype=torch.float32, device=DEV)
+    acc, shift = _acc(B * nq, maxn, Hq)
+    K.attention(q, out, pool, 0, items, B, maxn, nq, Hq, lse=lse, acc=acc, acc_row_stride=maxn, acc_shift=shift,
+                planted=torch.tensor(planted, dtype=torch.int32, device=DEV) if planted else None,
+                planted_bonus=1.5 if planted else 0.0)
+    torch.cuda.synchronize()
+    for r, n in enumerate(n0s):
+        kr, vr = pool.read(r, range(n + nq))
+        kr, vr = kr.double().cpu().numpy()[:, 0], vr.double().cpu().numpy()[:, 0]
+        sl = slice(r * nq, (r + 1) * nq)
+        ro, rl, ra = _ref_rows(q[sl].double().cpu().numpy(), kr, vr, Hq, Hkv, d, [], range(n + nq), n,
+                               planted=planted, bonus=1.5)
+        assert np.abs(out[sl].double().cpu().numpy() - ro).max() <= 2e-2, (r, n)
+        assert np.abs(lse[sl].double().cpu().numpy() - rl).max() <= 2e-2, (r, n)
+        a = _accf(acc[sl], shift)
+        for t in range(nq):
+            want = np.zeros(maxn)
+            for p_, val in ra[t].items():
+                want[p_] = val
+            assert np.abs(a[t] - want).max() <= 2e-2, (r, n, t)
+    return acc
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+@pytest.mark.parametrize("G", [4, 8])
+def test_verify_k_by_group_bf16(k, G):
+    """configs[4]'s verify envelope: k+1 tokens x GQA group rows (12 .. 72 -> NR 16 .. 72)
+    on the tcgen05 kernel, several items of different context in one launch."""
+    _verify_case([4096, 1500, 129, 3], k + 1, G, seed=100 * k + G)
+
+
+@pytest.mark.parametrize("G,n0", [(4, 20475), (4, 22000), (4, 1270), (8, 12283), (8, 13000), (4, 40000)])
+def test_verify_tmem_slot_edges_bf16(G, n0):
+    """Per-CTA tile counts at / just past the TMEM-resident slot count (the slot that doubles
+    as the O accumulator is consumed first), below it, and far past it (evicted tiles
+    recomputed)."""
+    _verify_case([n0], 5, G, Hkv=2, seed=n0, scale=0.5)
+
+
+def test_verify_single_token_bf16():
+    """Greedy-decode shape: one query token (4 or 8 rows -> NR 8) over a dense context."""
+    for G in (4, 8):
+        _verify_case([3000, 700], 1, G, seed=G)
+
+
+@pytest.mark.parametrize("G,rows", [(4, 48), (4, 64), (8, 48), (8, 80)])
+def test_prefill_chunks_share_one_score_row_bf16(G, rows):
+    """Prefill work items (BatchedDecoder._prefill_group): a 300-token prompt split into
+    windows of rows/G tokens, every window summing its scores into ONE accumulator row
+    (acc_step = 0, engine.py:192: all prompt rows count)."""
+    rng = np.random.default_rng(rows + G)
+    Hkv, d = 4, 128
+    Hq = Hkv * G
+    P = 300
+    pool = _pool(1, Hkv, d, P, 1, torch.bfloat16, shuffle_seed=2)
+    _fill(pool, 0, P, rng)
+    kr, vr = pool.read(0, range(P))
+    kr, vr = kr.double().cpu().numpy()[:, 0], vr.double().cpu().numpy()[:, 0]
+    step = rows // G
+    items = make_items([(0, q0, min(step, P - q0), q0, 0, 0, 0, 0, 0) for q0 in range(0, P, step)], DEV)
+    n_items = -(-P // step)
+    q = torch.from_numpy(rng.normal(size=(P, Hq, d))).to(DEV, torch.bfloat16)
+    out = torch.empty_like(q)
+    shift = K.score_shift(P, 1, Hq)
+    acc = torch.zeros(1, P, dtype=torch.int64, device=DEV)
+    K.attention(q, out, pool, 0, items, n_items, P, step, Hq, acc=acc, acc_row_stride=P, acc_shift=shift)
+    torch.cuda.synchronize()
+    ro, _, ra = _ref_rows(q.double().cpu().numpy(), kr, vr, Hq, Hkv, d, [], range(P), 0)
+    assert np.abs(out.double().cpu().numpy() - ro).max() <= 2e-2
+    want = np.zeros(P)
+    for t in range(P):
+        for p_, val in ra[t].items():
+            want[p_] += val
+    got = _accf(acc, shift)[0]
+    np.testing.assert_allclose(got.sum(), P * Hq, rtol=1e-2)
+    assert np.abs(got - want).max() <= 2e-2 * max(1.0, want.max())
+
+
+def test_score_accumulation_is_bitwise_deterministic_bf16():
+    """The fixed-point score reductions land in any order across heads and cluster CTAs;
+    the accumulated integers must not depend on it (repeat launches, bitwise)."""
+    rng = np.random.default_rng(9)
+    Hkv, G, d, nq = 8, 4, 128, 5
+    Hq = Hkv * G
+    lens = [6000, 3000, 8000, 100]
+    maxn = max(lens) + nq
+    pool = _pool(1, Hkv, d, maxn, len(lens), torch.bfloat16, shuffle_seed=3)
+    for r, n in enumerate(lens):
+        _fill(pool, r, n + nq, rng)
+    items = make_items([(r, r * nq, nq, n, 0, 0, 0, r * nq, 1) for r, n in enumerate(lens)], DEV)
+    q = torch.from_numpy(rng.normal(size=(len(lens) * nq, Hq, d))).to(DEV, torch.bfloat16)
+    out = torch.empty_like(q)
+    runs = []
+    for _ in range(4):
+        acc, shift = _acc(len(lens) * nq, maxn, Hq, L=36)
+        for layer_rep in range(3):  # several "layers" accumulate into the same rows
+            K.attention(q, out, pool, 0, items, len(lens), maxn, nq, Hq, acc=acc, acc_row_stride=maxn,
+                        acc_shift=shift)
+        runs.append(acc.cpu())
+    for r in runs[1:]:
+        assert torch.equal(r, runs[0])
+
+
+def test_rope_kv_write_bf16_matches_oracle():
+    """K5 bf16 branch: rotated q / k rounded to bf16 once, v copied exactly (model.py:212-222)."""
+    rng = np.random.default_rng(12)
+    Hq, Hkv, d, L = 16, 4, 128, 2
+    pool = _pool(L, Hkv, d, 9000, 2, torch.bfloat16)
+    rows = 7
+    qkv = torch.from_numpy(rng.normal(size=(rows, (Hq + 2 * Hkv) * d))).to(DEV, torch.bfloat16)
+    pos = np.array([0, 1, 17, 100, 4095, 8191, 8999], dtype=np.int32)
+    tab = np.array([0, 1, 0, 1, 1, 0, 1], dtype=np.int32)
+    q_out = torch.empty(rows, Hq, d, dtype=torch.bfloat16, device=DEV)
+    K.rope_kv_write(qkv, torch.from_numpy(tab).to(DEV), torch.from_numpy(pos).to(DEV), pool, 1, Hq, q_out)
+    torch.cuda.synchronize()
+    x = qkv.double().cpu().numpy()
+    for r in range(rows):
+        want_q = O.rope(x[r, : Hq * d].reshape(Hq, d), int(pos[r]), d)
+        want_k = O.rope(x[r, Hq * d:(Hq + Hkv) * d].reshape(Hkv, d), int(pos[r]), d)
+        want_v = x[r, (Hq + Hkv) * d:].reshape(Hkv, d)
+        kk, vv = pool.read(int(tab[r]), [int(pos[r])])
+        # one bf16 rounding of the fp32 rotation: |err| <= 2^-8 |x| + fp32 angle error at 9K positions
+        assert np.abs(q_out[r].double().cpu().numpy() - want_q).max() <= 1e-2 * max(1.0, np.abs(want_q).max())
+        assert np.abs(kk[0, 1].double().cpu().numpy() - want_k).max() <= 1e-2 * max(1.0, np.abs(want_k).max())
+        assert np.array_equal(vv[0, 1].double().cpu().numpy(), want_v)

@@ -35,7 +35,9 @@ def source_stamp() -> str:
     for f in sorted(HERE.glob("*.cu")) + sorted(HERE.glob("*.cuh")) + [ROOT / "include" / "spardec_b200.h"]:
         h.update(f.name.encode())
         h.update(f.read_bytes())
-    h.update(" ".join(FLAGS).encode())
+    # flags without the absolute include path: the id must not change when the tree moves
+    # (the GPU box runs the snapshot from another directory)
+    h.update(" ".join(f for f in FLAGS if not f.startswith("/")).encode())
     return h.hexdigest()
 
 

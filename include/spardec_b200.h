@@ -20,6 +20,9 @@
  *   sd_topk               selection.py:186-204 (select_critical_tokens)
  *   sd_argmax_rows        model.py:388-390 (greedy_token)
  *   sd_greedy_accept      engine.py:231-239 (verify_round accept loop + bonus)
+ *   sd_step_prepare /     one unified iteration with device-resident request state
+ *   sd_step_commit        (engine.py:196-260 per member; the delayed-verification
+ *                         pipeline of scheduler.py:135-197, simulate.py:353-451)
  *
  * Conventions
  *   - Plain pointers and sizes only; every pointer is device memory unless
@@ -57,6 +60,17 @@ extern "C" {
 #define SD_ITEM_ACC_ROW 7   /* first score-accumulator row, -1 = no score capture   */
 #define SD_ITEM_ACC_STEP 8  /* accumulator row step per query token (0 = sum rows)  */
 #define SD_ITEM_FIELDS 12
+
+/* One member of a unified iteration (int32 record of SD_PLAN_FIELDS), host -> device. */
+#define SD_PLAN_SLOT 0  /* request slot (block-table row, state index)             */
+#define SD_PLAN_KIND 1  /* SD_PLAN_DRAFT or SD_PLAN_VERIFY                          */
+#define SD_PLAN_ROW0 2  /* first row of the member in the iteration's row batch     */
+#define SD_PLAN_ROWS 3  /* 1 (draft) or round_target + 1 (verify)                   */
+#define SD_PLAN_PHASE 4 /* draft step within the round (draft members)              */
+#define SD_PLAN_ITEM 5  /* index into the draft / verify work items (and results)   */
+#define SD_PLAN_FIELDS 6
+#define SD_PLAN_DRAFT 0
+#define SD_PLAN_VERIFY 1
 
 /* Paged KV pool.  K and V: [layers][num_slots][kv_heads][head_dim] of dtype.
  * Logical position p of table row r lives in slot
@@ -152,6 +166,26 @@ int sd_argmax_rows(const void* logits, int32_t dtype, int64_t row_stride, int32_
 int sd_greedy_accept(const int32_t* targets, const int32_t* tokens, const int32_t* row0,
                      const int32_t* nrows, int32_t num, int32_t* accepted, int32_t* bonus,
                      void* stream);
+
+/* Unified iteration, device side (no host round trip between iterations).
+ * Device state per request slot: n_kv[slot] committed KV rows, last_tok[slot] the
+ * pending token (committed[-1]), drafted[slot][k] this round's drafts.
+ * sd_step_prepare: from plan[n_members][SD_PLAN_FIELDS] writes the iteration's input
+ *   tokens / row_table / row_pos, the verify work items v_items[...] (score capture into
+ *   acc rows slot*(k+1)+j, zeroed here over [0, n_kv + rows)) and the draft work items
+ *   d_items[...] (critical list at crit + slot*crit_cap, crit_len[slot], fresh tail from
+ *   n_kv[slot]) (engine.py:196-231, model.py:360-365).
+ * sd_step_commit (after sd_argmax_rows into targets[rows]): drafts store their target
+ *   in drafted[slot][phase]; verifies apply the accept rule (engine.py:231-240), roll
+ *   back n_kv += a + 1, set last_tok = bonus, write sel_rows/sel_kv/sel_slot[item] (the
+ *   sd_select_critical inputs) and results[item][k+2] = {a, bonus, drafted[0..k-1]}. */
+int sd_step_prepare(const int32_t* plan, int32_t n_members, int32_t k, int32_t crit_cap, const int32_t* n_kv,
+                    const int32_t* last_tok, const int32_t* drafted, const int32_t* crit_len, int32_t* tokens,
+                    int32_t* row_table, int32_t* row_pos, int32_t* v_items, int32_t* d_items, uint64_t* acc,
+                    int64_t acc_row_stride, void* stream);
+int sd_step_commit(const int32_t* plan, int32_t n_members, int32_t k, const int32_t* targets, int32_t* n_kv,
+                   int32_t* last_tok, int32_t* drafted, int32_t* sel_rows, int32_t* sel_kv, int32_t* sel_slot,
+                   int32_t* results, void* stream);
 
 /* Glue (outside the attention hot path): out = x / sqrt(mean(x^2) + eps) per
  * row (model.py:225-226, RMSNorm without gain) cast to out_dtype.  x fp32. */

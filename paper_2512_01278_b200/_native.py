@@ -20,6 +20,8 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libspardec_b200.so"
 SD_DTYPE_F32 = 0
 SD_DTYPE_BF16 = 1
 ITEM_FIELDS = 12
+PLAN_FIELDS = 6   # SD_PLAN_FIELDS
+PLAN_DRAFT, PLAN_VERIFY = 0, 1
 (F_TABLE_ROW, F_Q_ROW0, F_NQ, F_QPOS0, F_CRIT_OFF, F_CRIT_LEN, F_DENSE_LO, F_ACC_ROW, F_ACC_STEP) = range(9)
 
 _c_p = ctypes.c_void_p
@@ -63,6 +65,9 @@ SIGNATURES = {
     "sd_topk": (ctypes.c_int, [_c_p, _i32, _i64, _c_p, _c_p, _i32, _c_p, _i64, _c_p, _c_p]),
     "sd_argmax_rows": (ctypes.c_int, [_c_p, _i32, _i64, _i32, _i32, _c_p, _c_p]),
     "sd_greedy_accept": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i32, _c_p, _c_p, _c_p]),
+    "sd_step_prepare": (ctypes.c_int, [_c_p, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                       _c_p, ctypes.c_int64, _c_p]),
+    "sd_step_commit": (ctypes.c_int, [_c_p, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
     "sd_rmsnorm_cast": (ctypes.c_int, [_c_p, _i32, _i32, ctypes.c_float, _c_p, _i32, _c_p]),
     "sd_forward_layers": (ctypes.c_int, [ctypes.POINTER(LayerWeights), _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                                          _i32, _i32, _i32, _c_p, _c_p, ctypes.POINTER(PagedKvDesc),

@@ -3,6 +3,10 @@
 // the launch planner that picks the cluster split.
 #include "attn_umma.cuh"
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 namespace sd {
 namespace umma_attn {
 
@@ -430,7 +434,8 @@ static int chunk_cap_tiles(int NR, int nslot, int S, int budget, int dense) {
 // (32 KB fills per CTA + a fixed per-CTA cost in fills, fitted to traced C sweeps).  Chunks
 // longer than the S TMEM-resident tiles re-read the evicted tiles' K in phase 2
 // (fills = 3*ct - S instead of 2*ct).
-static bool plan_umma(int max_keys, int num_items, int kv_heads, int S, int cap, int slots, int* C_out,
+template <typename SlotsFn>
+static bool plan_umma(int max_keys, int num_items, int kv_heads, int S, int cap, SlotsFn slots_of, int* C_out,
                       int* chunk_out, int dense) {
   using namespace umma_attn;
   const int tiles = (max_keys + TK - 1) / TK;
@@ -448,6 +453,8 @@ static bool plan_umma(int max_keys, int num_items, int kv_heads, int S, int cap,
     if (ct > cap) continue;
     const double fills = ct <= S ? 2.0 * ct : 3.0 * ct - S;
     const long long ctas = work * c;
+    const int slots = slots_of(c, ct);
+    if (slots <= 0) continue;
     const double waves = (double)((ctas + slots - 1) / slots);
     const double cost = waves * (fills + ovh);
     if (cost < best_cost * 0.98) best_cost = cost, best = c;
@@ -477,10 +484,37 @@ static bool umma_plan(const sd_paged_kv* kvp, int num_items, int max_keys, int m
   const int S = tcols / NR;
   const int cap = chunk_cap_tiles(NR, nslot, S, narrow ? 113 * 1024 : 227 * 1024, dense);
   int C = 1, chunk = TK;
-  if (cap == 0 || !plan_umma(max_keys < 1 ? 1 : max_keys, num_items, kvp->kv_heads, S, cap, narrow ? 296 : 148,
-                             &C, &chunk, dense))
+  // CTA slots per cluster size, from the occupancy API (cached per shape)
+  auto slots_of = [&](int c, int ct) -> int {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, int, int>, int> cache;
+    const int smem = make_layout(NR, nslot, S, ct, dense).total;
+    const auto key = std::make_tuple(G, NR, c, smem, dense);
+    std::lock_guard<std::mutex> lock(mu);
+    auto itc = cache.find(key);
+    if (itc != cache.end()) return itc->second;
+    int v = G == 4 ? verify_slots_g4(NR, c, smem) : verify_slots_g8(NR, c, smem);
+    if (v <= 0) v = 0;
+    cache[key] = v;
+    return v;
+  };
+  if (cap == 0 || !plan_umma(max_keys < 1 ? 1 : max_keys, num_items, kvp->kv_heads, S, cap, slots_of, &C, &chunk,
+                             dense))
     return false;
   pl->NR = NR, pl->C = C, pl->chunk = chunk;
+  static const int log_plan = env_int("SD_ATTN_PLAN_LOG", 0);
+  if (log_plan > 1) {
+    static bool once = false;
+    if (!once) {
+      once = true;
+      for (int c = 1; c <= 16; ++c)
+        for (int ct : {1, 8, 32})
+          fprintf(stderr, "[sd slots] G=%d NR=%d C=%d ct=%d slots=%d\n", G, NR, c, ct, slots_of(c, ct));
+    }
+  }
+  if (log_plan)
+    fprintf(stderr, "[sd plan] items=%d keys=%d NR=%d C=%d chunk_tiles=%d slots=%d dense=%d\n", num_items, max_keys,
+            NR, C, chunk / TK, slots_of(C, chunk / TK), dense);
   return true;
 }
 

@@ -581,19 +581,56 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
   verify_body<G, NR, NSLOT, TCOLS>(p, blockIdx.y, blockIdx.z);
 }
 
+// dynamic shared memory / cluster attributes of one instantiation (raised on demand)
+template <int G, int NR, int NSLOT, int TCOLS>
+void configure_verify(int smem) {
+  static int configured = 0;
+  if (smem > configured) {
+    auto kern = attn_umma_kernel<G, NR, NSLOT, TCOLS>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    configured = smem;
+  }
+}
+
+// CTA slots the GPU offers C-CTA clusters of this instantiation at once: clusters live
+// inside one GPC, so for C that do not divide a GPC's CTA slots this is well below
+// 148 x CTAs-per-SM (the planner's wave count uses it)
+template <int G, int NR, int NSLOT, int TCOLS>
+int verify_slots(int C, int smem) {
+  configure_verify<G, NR, NSLOT, TCOLS>(smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (getenv("SD_ATTN_PLAN_LOG") && C == 1) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_umma_kernel<G, NR, NSLOT, TCOLS>, NT, smem);
+    fprintf(stderr, "[sd slots] NR=%d smem=%d blocks/SM=%d\n", NR, smem, per_sm);
+  }
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, attn_umma_kernel<G, NR, NSLOT, TCOLS>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return clusters * C;
+}
+
 // launch one verify grid (C-CTA clusters) of attn_umma_kernel<G, NR, NSLOT, TCOLS>
 template <int G, int NR, int NSLOT, int TCOLS>
 int launch_verify(const Params& prm, int C, int num_items, int kv_heads, cudaStream_t stream) {
   constexpr int S = TCOLS / NR;
   auto kern = attn_umma_kernel<G, NR, NSLOT, TCOLS>;
   const int smem = make_layout(NR, NSLOT, S, prm.chunk / TK, prm.dense).total;
-  static int configured = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    configured = smem;
-  }
+  configure_verify<G, NR, NSLOT, TCOLS>(smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C, kv_heads, num_items);
   cfg.blockDim = dim3(NT);
@@ -621,6 +658,8 @@ constexpr int kNarrowMaxNR = 48;
 constexpr int kMaxNR = 80;
 int launch_verify_g4(const Params& prm, int NR, int C, int num_items, int kv_heads, cudaStream_t stream);
 int launch_verify_g8(const Params& prm, int NR, int C, int num_items, int kv_heads, cudaStream_t stream);
+int verify_slots_g4(int NR, int C, int smem);
+int verify_slots_g8(int NR, int C, int smem);
 
 }  // namespace umma_attn
 }  // namespace sd

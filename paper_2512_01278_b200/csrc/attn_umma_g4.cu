@@ -5,22 +5,31 @@
 namespace sd {
 namespace umma_attn {
 
+#define SD_VERIFY_SHAPES(X) \
+  X(8, 2, 256) X(16, 2, 256) X(24, 2, 256) X(32, 2, 256) X(40, 2, 256) X(48, 2, 256) \
+  X(56, 4, 512) X(64, 4, 512) X(72, 4, 512) X(80, 4, 512)
+
 int launch_verify_g4(const Params& prm, int NR, int C, int num_items, int kv_heads, cudaStream_t stream) {
   switch (NR) {
-    case 8: return launch_verify<4, 8, 2, 256>(prm, C, num_items, kv_heads, stream);
-    case 16: return launch_verify<4, 16, 2, 256>(prm, C, num_items, kv_heads, stream);
-    case 24: return launch_verify<4, 24, 2, 256>(prm, C, num_items, kv_heads, stream);
-    case 32: return launch_verify<4, 32, 2, 256>(prm, C, num_items, kv_heads, stream);
-    case 40: return launch_verify<4, 40, 2, 256>(prm, C, num_items, kv_heads, stream);
-    case 48: return launch_verify<4, 48, 2, 256>(prm, C, num_items, kv_heads, stream);
-    case 56: return launch_verify<4, 56, 4, 512>(prm, C, num_items, kv_heads, stream);
-    case 64: return launch_verify<4, 64, 4, 512>(prm, C, num_items, kv_heads, stream);
-    case 72: return launch_verify<4, 72, 4, 512>(prm, C, num_items, kv_heads, stream);
-    case 80: return launch_verify<4, 80, 4, 512>(prm, C, num_items, kv_heads, stream);
+#define X(nr, ns, tc) \
+  case nr: return launch_verify<4, nr, ns, tc>(prm, C, num_items, kv_heads, stream);
+    SD_VERIFY_SHAPES(X)
+#undef X
     default: break;
   }
   set_error("sd_attention (umma): no verify kernel for NR = " + std::to_string(NR));
   return -1;
+}
+
+int verify_slots_g4(int NR, int C, int smem) {
+  switch (NR) {
+#define X(nr, ns, tc) \
+  case nr: return verify_slots<4, nr, ns, tc>(C, smem);
+    SD_VERIFY_SHAPES(X)
+#undef X
+    default: break;
+  }
+  return 0;
 }
 
 }  // namespace umma_attn

@@ -21,7 +21,7 @@ ROOT = PKG.parent
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libspardec_b200.so"
 SOURCES = ["abi.cu", "attn_generic.cu", "rope_kv.cu", "select.cu", "accept.cu", "glue.cu", "attn_umma.cu",
-           "attn_umma_g4.cu", "attn_umma_g8.cu", "forward.cu"]
+           "attn_umma_g4.cu", "attn_umma_g8.cu", "forward.cu", "pipeline.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -141,6 +141,26 @@ def greedy_accept(targets: torch.Tensor, tokens: torch.Tensor, row0: torch.Tenso
             "sd_greedy_accept")
 
 
+def step_prepare(plan: torch.Tensor, n_members: int, k: int, crit_cap: int, n_kv: torch.Tensor,
+                 last_tok: torch.Tensor, drafted: torch.Tensor, crit_len: torch.Tensor, tokens: torch.Tensor,
+                 row_table: torch.Tensor, row_pos: torch.Tensor, v_items: torch.Tensor, d_items: torch.Tensor,
+                 acc: torch.Tensor, acc_row_stride: int) -> None:
+    """Iteration inputs (tokens, positions, work items) from the device-resident request state."""
+    N.check(N.lib().sd_step_prepare(plan.data_ptr(), n_members, k, crit_cap, n_kv.data_ptr(), last_tok.data_ptr(),
+                                    drafted.data_ptr(), crit_len.data_ptr(), tokens.data_ptr(), row_table.data_ptr(),
+                                    row_pos.data_ptr(), v_items.data_ptr(), d_items.data_ptr(), acc.data_ptr(),
+                                    acc_row_stride, N.stream_handle()), "sd_step_prepare")
+
+
+def step_commit(plan: torch.Tensor, n_members: int, k: int, targets: torch.Tensor, n_kv: torch.Tensor,
+                last_tok: torch.Tensor, drafted: torch.Tensor, sel_rows: torch.Tensor, sel_kv: torch.Tensor,
+                sel_slot: torch.Tensor, results: torch.Tensor) -> None:
+    """Drafts record their token; verifies accept / roll back on the device (engine.py:231-240)."""
+    N.check(N.lib().sd_step_commit(plan.data_ptr(), n_members, k, targets.data_ptr(), n_kv.data_ptr(),
+                                   last_tok.data_ptr(), drafted.data_ptr(), sel_rows.data_ptr(), sel_kv.data_ptr(),
+                                   sel_slot.data_ptr(), results.data_ptr(), N.stream_handle()), "sd_step_commit")
+
+
 def rmsnorm_cast(x: torch.Tensor, out: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:
     """Glue: RMSNorm without gain of fp32 rows, cast to out.dtype (one launch)."""
     if x.dtype != torch.float32 or not x.is_contiguous() or not out.is_contiguous():

@@ -392,9 +392,10 @@ class KVEntry:
     v: torch.Tensor
 
     def validate(self) -> None:
-        if self.k.shape != self.v.shape or self.k.dim() != 3:
+        k, v = torch.as_tensor(self.k), torch.as_tensor(self.v)
+        if k.shape != v.shape or k.dim() != 3:
             raise ContractError("KV entry arrays must share a (layers, heads, dim) shape")
-        if not (bool(torch.isfinite(self.k).all()) and bool(torch.isfinite(self.v).all())):
+        if not (bool(torch.isfinite(k).all()) and bool(torch.isfinite(v).all())):
             raise ContractError("KV entry contains non-finite values")
 
 
@@ -405,10 +406,13 @@ class KvCache:
 
     PAGE = 16
 
-    def __init__(self, config: ModelConfig, capacity: int = 16, dtype: torch.dtype = torch.float32,
+    def __init__(self, config: ModelConfig, capacity: int = 16, dtype: torch.dtype | None = None,
                  device="cuda"):
         self.config = config
-        self.dtype = dtype
+        # the reference's KvCache(config, capacity) has no dtype: without one, an empty cache
+        # takes the dtype of the first model that runs a forward over it (adopt_dtype)
+        self._auto_dtype = dtype is None
+        self.dtype = torch.float32 if dtype is None else dtype
         self.device = torch.device(device)
         self._n = 0
         self._pool = self._new_pool(max(capacity, 1))
@@ -425,6 +429,13 @@ class KvCache:
     @property
     def pool(self) -> PagedKvPool:
         return self._pool
+
+    def adopt_dtype(self, dtype: torch.dtype) -> None:
+        """Switch an empty, dtype-less cache to ``dtype`` (no-op otherwise)."""
+        if self._auto_dtype and self._n == 0 and dtype != self.dtype:
+            cap = self.capacity
+            self.dtype = dtype
+            self._pool = self._new_pool(cap)
 
     @property
     def capacity(self) -> int:
@@ -476,6 +487,7 @@ def _check_tokens(config: ModelConfig, tokens: Sequence[int]) -> None:
 
 
 def _require_cache_dtype(model: ToyModel, cache: KvCache) -> None:
+    cache.adopt_dtype(model.dtype)
     if cache.dtype != model.dtype:
         raise ContractError(f"cache dtype {cache.dtype} != model dtype {model.dtype}")
 

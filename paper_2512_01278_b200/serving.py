@@ -54,10 +54,27 @@ class Seq:
     budget: int = 0
     done: bool = False
     stats: RoundStats | None = None
+    inflight: bool = False   # a submitted verification whose outcome the host has not applied
+    n_kv_ub: int = 0         # upper bound of n_kv while inflight
 
     @property
     def kv_len(self) -> int:
         return len(self.prompt) + len(self.committed) + len(self.drafted)
+
+
+@dataclass
+class PendingStep:
+    """A submitted iteration (BatchedDecoder.submit) awaiting BatchedDecoder.complete."""
+
+    index: int
+    ring: int
+    verifs: list     # (seq, drafted count, kv_len at verify, budget of the round's set)
+    drafts: list
+    rows: int
+    draft_rows: int
+    event: object
+    t_host0: float
+    t_launched: float
 
 
 @dataclass
@@ -94,6 +111,31 @@ class BatchedDecoder:
         self.imp = torch.zeros(max_requests, self.acc_w, dtype=torch.float64, device=self.dev)
         self.verify_shift = K.score_shift(1, c.num_layers, c.num_q_heads)
         self.prefill_shift = K.score_shift(self.max_seq_len, c.num_layers, c.num_q_heads)  # prompt rows sum
+        # device-resident request state (csrc/pipeline.cu): the iteration's inputs are built and
+        # its accept/rollback applied on the device, so the host can enqueue iteration i+1
+        # before it reads iteration i's results (delayed verification processing)
+        self.n_kv_dev = torch.zeros(max_requests, dtype=torch.int32, device=self.dev)
+        self.last_tok_dev = torch.zeros(max_requests, dtype=torch.int32, device=self.dev)
+        self.drafted_dev = torch.zeros(max_requests, k, dtype=torch.int32, device=self.dev)
+        max_rows = max_requests * (k + 1)
+        self._tok_buf = torch.zeros(max_rows, dtype=torch.int32, device=self.dev)
+        self._rt_buf = torch.zeros(max_rows, dtype=torch.int32, device=self.dev)
+        self._rp_buf = torch.zeros(max_rows, dtype=torch.int32, device=self.dev)
+        self._targets = torch.zeros(max_rows, dtype=torch.int32, device=self.dev)
+        self._v_items = torch.zeros(max_requests, N.ITEM_FIELDS, dtype=torch.int32, device=self.dev)
+        self._d_items = torch.zeros(max_requests, N.ITEM_FIELDS, dtype=torch.int32, device=self.dev)
+        self._sel = torch.zeros(3, max_requests, dtype=torch.int32, device=self.dev)
+        self._res_dev = torch.zeros(max_requests, k + 2, dtype=torch.int32, device=self.dev)
+        self._plan_dev = torch.zeros(max_requests, N.PLAN_FIELDS, dtype=torch.int32, device=self.dev)
+        # pinned host rings: a plan buffer may be rewritten only after its H2D copy ran, a
+        # result buffer is read after its D2H copy's event
+        self._ring = 3
+        self._plan_host = [torch.zeros(max_requests, N.PLAN_FIELDS, dtype=torch.int32, pin_memory=True)
+                           for _ in range(self._ring)]
+        self._res_host = [torch.zeros(max_requests, k + 2, dtype=torch.int32, pin_memory=True)
+                          for _ in range(self._ring)]
+        self._ring_ev = [None] * self._ring
+        self._iter = 0
         self.free_slots = list(range(max_requests - 1, -1, -1))
         self.seqs: dict = {}
         self._host_kv: dict = {}     # request -> {position: (K rows, V rows)} pinned host copies
@@ -240,6 +282,8 @@ class BatchedDecoder:
             s.n_kv = len(pr)
             if not s.done:
                 refresh.append((s, 1))
+        self.n_kv_dev.index_copy_(0, _i32([s.slot for s in seqs], self.dev).long(),
+                                  _i32([s.n_kv for s in seqs], self.dev))
         self._refresh(refresh, self.prefill_shift)
         return seqs
 
@@ -267,7 +311,11 @@ class BatchedDecoder:
                             acc_row_stride=self.acc_w, acc_shift=shift)
         x = forward_rows(self.model, self.pool, tok, _i32(rt, self.dev), _i32(rp, self.dev), [launch])
         last = torch.tensor(np.cumsum([len(s.prompt) for s in seqs]) - 1, device=self.dev)
-        first = _argmax(lm_head(self.model, x.index_select(0, last))).cpu().tolist()
+        first_dev = _argmax(lm_head(self.model, x.index_select(0, last)))
+        slots_dev = _i32([s.slot for s in seqs], self.dev).long()
+        self.last_tok_dev.index_copy_(0, slots_dev, first_dev)
+        self.n_kv_dev.index_copy_(0, slots_dev, _i32([len(s.prompt) for s in seqs], self.dev))
+        first = first_dev.cpu().tolist()
         refresh = []
         for s, t in zip(seqs, first):
             s.n_kv = len(s.prompt)
@@ -295,96 +343,123 @@ class BatchedDecoder:
     # -- one unified iteration --------------------------------------------------------------
     def step(self, draft_ids, verify_ids) -> StepResult:
         """Run every draft member one draft step and every verify member its
-        verification, as one batched forward (engine.py:196-260 semantics)."""
+        verification, as one batched forward (engine.py:196-260 semantics), and
+        process the results before returning (synchronous pipeline)."""
+        return self.complete(self.submit(draft_ids, verify_ids))
+
+    def submit(self, draft_ids, verify_ids) -> "PendingStep":
+        """Enqueue one unified iteration without waiting for any device result.
+
+        Input tokens, positions and work items come from the device-resident request
+        state (sd_step_prepare); accept / rollback / critical refresh run on the device
+        (sd_step_commit, K3).  The host mirrors only what scheduling needs: draft
+        phases advance here, verify outcomes (accepted count, bonus, emitted tokens,
+        done) arrive with ``complete`` — typically called for iteration i after
+        iteration i+1 has been submitted (delayed verification processing,
+        scheduler.py:135-197), which keeps the GPU busy while the host works."""
         c = self.model.config
         t_host0 = time.perf_counter()
-        toks, rt, rp = [], [], []
-        d_items, v_items = [], []
         drafts = [self.seqs[r] for r in draft_ids]
         verifs = [self.seqs[r] for r in verify_ids]
+        n_members = len(drafts) + len(verifs)
+        j = self._iter % self._ring
+        self._iter += 1
+        if self._ring_ev[j] is not None:
+            self._ring_ev[j].synchronize()   # its plan copy and result copy are done
+        plan = self._plan_host[j].numpy()
         row = 0
         d_max_keys = 1
-        for s in drafts:
+        for i, s in enumerate(drafts):
             if s.done or s.phase >= s.round_target:
                 raise ContractError(f"request {s.request_id} cannot draft now")
-            tok = s.drafted[-1] if s.drafted else s.committed[-1]
-            pos = s.n_kv + s.phase
-            toks.append(tok)
-            rt.append(s.slot)
-            rp.append(pos)
-            d_items.append((s.slot, row, 1, pos, s.slot * self.crit_cap, s.crit_len, s.n_kv, -1, 0))
-            d_max_keys = max(d_max_keys, s.crit_len + s.phase + 1)
+            plan[i] = (s.slot, N.PLAN_DRAFT, row, 1, s.phase, i, )
+            # an upper bound while the previous verify's outcome is still in flight
+            n_kv = s.n_kv_ub if s.inflight else s.n_kv
+            crit = min(compute_budget(n_kv, self.sparsity), n_kv) if s.inflight else s.crit_len
+            d_max_keys = max(d_max_keys, crit + s.phase + 1)
             row += 1
         n_draft_rows = row
-        v_row0, v_n = [], []
         v_max_keys, v_max_nq = 1, 1
-        for s in verifs:
+        vinfo = []
+        for m, s in enumerate(verifs):
             if s.done or s.phase != s.round_target:
                 raise ContractError(f"request {s.request_id} cannot verify now")
-            seq_toks = [s.committed[-1], *s.drafted]
-            t = len(seq_toks)
-            toks.extend(seq_toks)
-            rt.extend([s.slot] * t)
-            rp.extend(range(s.n_kv, s.n_kv + t))
-            v_items.append((s.slot, row, t, s.n_kv, 0, 0, 0, s.slot * (self.k + 1), 1))
-            v_row0.append(row)
-            v_n.append(t)
+            if s.inflight:
+                raise ContractError(f"request {s.request_id}: previous verification not processed yet")
+            t = s.round_target + 1
+            plan[len(drafts) + m] = (s.slot, N.PLAN_VERIFY, row, t, 0, m)
             v_max_keys = max(v_max_keys, s.n_kv + t)
             v_max_nq = max(v_max_nq, t)
+            vinfo.append((s, len(s.drafted), s.kv_len, s.budget))
             row += t
         R = row
         if R == 0:
-            return StepResult({}, 0, 0, 0, 0)
+            return PendingStep(self._iter - 1, j, [], [], 0, 0, None, t_host0, time.perf_counter())
+        plan_dev = self._plan_dev[:n_members]
+        plan_dev.copy_(self._plan_host[j][:n_members], non_blocking=True)
+        K.step_prepare(plan_dev, n_members, self.k, self.crit_cap, self.n_kv_dev, self.last_tok_dev,
+                       self.drafted_dev, self.crit_len_dev, self._tok_buf, self._rt_buf, self._rp_buf,
+                       self._v_items, self._d_items, self.acc, self.acc.stride(0))
         launches = []
-        if v_items:
-            slots = torch.tensor([s.slot for s in verifs], device=self.dev)
-            self.acc.view(self.max_requests, self.k + 1, self.acc_w)[slots] = 0
-            launches.append(AttnLaunch(_items(v_items, self.dev), len(v_items), v_max_keys, v_max_nq, acc=self.acc,
+        if verifs:
+            launches.append(AttnLaunch(self._v_items, len(verifs), v_max_keys, v_max_nq, acc=self.acc,
                                        acc_row_stride=self.acc_w, acc_shift=self.verify_shift,
                                        timer=self._timer("verify")))
-        if d_items:  # after the verify launch: it runs on the side stream (model.forward_rows)
-            launches.append(AttnLaunch(_items(d_items, self.dev), len(d_items), d_max_keys, 1, crit=self.crit,
+        if drafts:  # after the verify launch: it runs on the side stream (model.forward_rows)
+            launches.append(AttnLaunch(self._d_items, len(drafts), d_max_keys, 1, crit=self.crit,
                                        timer=self._timer("draft")))
-        tok_dev = _i32(toks, self.dev)
-        x = forward_rows(self.model, self.pool, tok_dev, _i32(rt, self.dev), _i32(rp, self.dev), launches)
-        targets = _argmax(lm_head(self.model, x))
-        t_launched = time.perf_counter()
+        x = forward_rows(self.model, self.pool, self._tok_buf[:R], self._rt_buf[:R], self._rp_buf[:R], launches)
+        targets = self._targets[:R]
+        K.argmax_rows(lm_head(self.model, x).contiguous(), targets)
+        sel_rows, sel_kv, sel_slot = self._sel[0], self._sel[1], self._sel[2]
+        K.step_commit(plan_dev, n_members, self.k, targets, self.n_kv_dev, self.last_tok_dev, self.drafted_dev,
+                      sel_rows, sel_kv, sel_slot, self._res_dev)
         if verifs:
-            row0_d, n_d = _i32(v_row0, self.dev), _i32(v_n, self.dev)
-            acc_d = torch.empty(len(verifs), dtype=torch.int32, device=self.dev)
-            bonus_d = torch.empty_like(acc_d)
-            K.greedy_accept(targets, tok_dev, row0_d, n_d, acc_d, bonus_d)
-            host = torch.cat([targets, acc_d, bonus_d]).cpu().numpy()
-        else:
-            host = targets.cpu().numpy()
-        t_synced = time.perf_counter()
-        self.host_times.append((t_launched - t_host0, t_synced - t_host0))
-        tg = host[:R]
-        emitted = 0
-        for i, s in enumerate(drafts):
-            s.drafted.append(int(tg[i]))
+            # K3 straight from the device accept results (engine.py:256-259)
+            K.select_critical(self.acc, (self.k + 1) * self.acc.stride(0), self.acc.stride(0), self.verify_shift,
+                              sel_rows, sel_kv, self.sparsity, len(verifs), self.imp, self.crit, self.crit_len_dev,
+                              req_index=sel_slot)
+            self._res_host[j][: len(verifs)].copy_(self._res_dev[: len(verifs)], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.dev))
+        self._ring_ev[j] = ev
+        # host mirror of the deterministic part of the state machine
+        for s in drafts:
+            s.drafted.append(None)   # the token itself lives in drafted_dev until the verify
             s.phase += 1
             s.stats.sparse_forwards += 1
+        for s, _, _, _ in vinfo:
+            s.n_kv_ub = s.n_kv + s.round_target + 1
+            s.inflight = True
+            s.drafted, s.phase, s.round_target = [], 0, self.k
+        return PendingStep(self._iter - 1, j, vinfo, drafts, R, n_draft_rows, ev, t_host0, time.perf_counter())
+
+    def complete(self, pend: "PendingStep") -> StepResult:
+        """Wait for a submitted iteration and apply its verify outcomes on the host:
+        emissions (engine.py:126-144), round records, KV length, next critical-set size."""
+        if pend.event is None:
+            return StepResult({}, 0, 0, 0, 0)
+        pend.event.synchronize()
+        t_synced = time.perf_counter()
+        self.host_times.append((pend.t_launched - pend.t_host0, t_synced - pend.t_host0))
+        res = self._res_host[pend.ring][: len(pend.verifs)].numpy()
+        emitted = 0
         accepted = {}
-        refresh = []
-        for m, s in enumerate(verifs):
-            a = int(host[R + m])
-            bonus = int(host[R + len(verifs) + m])
-            kv_at = s.kv_len
-            drafts_m = s.drafted
+        for m, (s, n_drafted, kv_at, budget) in enumerate(pend.verifs):
+            a, bonus = int(res[m, 0]), int(res[m, 1])
+            drafts_m = [int(t) for t in res[m, 2:2 + n_drafted]]
             s.n_kv += a + 1  # KV rollback: rows beyond n_kv + a are dead
+            s.inflight = False
             landed = self._emit(s, drafts_m[:a] + [bonus])
             emitted += landed
             s.stats.emitted_tokens += landed
             s.stats.full_forwards += 1
-            s.stats.rounds.append(RoundRecord(len(s.stats.rounds), len(drafts_m), a, kv_at, s.budget))
-            s.drafted, s.phase, s.round_target = [], 0, self.k
+            s.stats.rounds.append(RoundRecord(len(s.stats.rounds), n_drafted, a, kv_at, budget))
             accepted[s.request_id] = a
-            if not s.done:
-                refresh.append((s, a + 1))
-        self._refresh(refresh, self.verify_shift)
-        self.last_rows = R
-        return StepResult(accepted, emitted, R, n_draft_rows, R - n_draft_rows)
+            s.budget = compute_budget(s.n_kv, self.sparsity)
+            s.crit_len = min(s.budget, s.n_kv)
+        self.last_rows = pend.rows
+        return StepResult(accepted, emitted, pend.rows, pend.draft_rows, pend.rows - pend.draft_rows)
 
     def _timer(self, kind):
         if self.attn_timer is None:

@@ -1,19 +1,24 @@
 """bf16 production shapes (head dim 128, GQA 4 and 8) through the drop-in API
 with real-length prompts, against the CPU oracle.
 
-The oracle runs in fp64 on the SAME bf16-rounded weights (our bf16 model's
-matrices widened to fp64), so the only difference is the arithmetic precision
-of the GPU path: bf16 operands, fp32 accumulation.  Tolerances (stated here,
-north_star: 2e-2 max-abs for bf16 attention):
+The oracle runs on the SAME bf16-rounded weights (our bf16 model's matrices
+widened to fp64) in two forms:
 
-  * K/V rows written by the GPU forward: max-abs <= 2e-2 * max(1, |ref|max)
-  * logits of every prompt row:          max-abs <= 3e-2 * max(1, |ref|max)
-    (two bf16 layers plus the bf16 LM head on top of the attention error)
-  * importance (normalised score mass):  max-abs <= 2e-2 * max(importance)
-  * greedy token streams: identical to the oracle's up to the first step where
-    the oracle's own top-1 / top-2 logit margin is below the logit tolerance
-    (a near tie that bf16 cannot resolve); the spec-decode stream always equals
-    the same-precision greedy stream (lossless).
+  * ``bf16=True``: the reference arithmetic with the bf16 data path's rounding
+    points (bf16 activations into every GEMM, bf16 K/V, P rounded to bf16 before
+    the PV product, fp32 residual stream) evaluated in fp64 — what the GPU
+    should compute up to fp32 accumulation order.  K/V rows and importance are
+    held to the north_star's bf16 tolerance, 2e-2 max-abs relative to
+    max(1, |ref|max); logits (two layers + LM head later) to 3e-2;
+  * plain fp64: this random-init model is badly conditioned (logit std ~6.5
+    at sigma 0.08, h = 1024), so bf16 rounding alone moves the logits by
+    several percent; the GPU must be no further from fp64 than 1.5x the
+    bf16-emulated path itself is.
+
+Greedy token streams: identical to the bf16 oracle's up to the first step where
+that oracle's own top-1 / top-2 logit margin is below the logit tolerance (a
+near tie that accumulation order can flip); the spec-decode stream always
+equals the same-precision greedy stream (lossless).
 
 Prompts are 512 tokens (configs[1]'s prompt length): the forward runs as
 48-row causal work items on the tcgen05 verify kernel (model.ITEM_ROWS).
@@ -73,10 +78,10 @@ def test_forward_full_512_prompt_matches_oracle(shp):
     torch.cuda.synchronize()
     assert len(cache) == 0
     assert K.launch_count() > launches0  # through the library
-    ref_logits, ref_k, ref_v, ref_scores = O.full_forward(w, O.Kv(w.shape), prompt)
+    ref_logits, ref_k, ref_v, ref_scores = O.full_forward(w, O.Kv(w.shape), prompt, bf16=True)
     got = torch.stack([r.float() for r in logits]).double().cpu().numpy() if isinstance(logits, list) \
         else logits.double().cpu().numpy()
-    _close(got, ref_logits, LOGIT_TOL, "prompt logits")
+    _close(got, ref_logits, LOGIT_TOL, "prompt logits vs bf16 oracle")
     gk = torch.stack([e.k for e in entries]).double().cpu().numpy()
     gv = torch.stack([e.v for e in entries]).double().cpu().numpy()
     _close(gk, ref_k, KV_TOL, "K rows")
@@ -85,17 +90,22 @@ def test_forward_full_512_prompt_matches_oracle(shp):
     imp = S.importance_from_log(log, len(prompt)).cpu().numpy()
     ref_imp = O.importance_grouped(ref_scores, len(prompt), len(prompt), shp[1], shp[2])
     assert float(np.abs(imp - ref_imp).max()) <= 2e-2 * float(ref_imp.max())
+    # against plain fp64: no worse than the bf16 data path itself
+    f64_logits, _, _, _ = O.full_forward(w, O.Kv(w.shape), prompt, keep_scores=False)
+    err_gpu = float(np.abs(got - f64_logits).max())
+    err_emul = float(np.abs(ref_logits - f64_logits).max())
+    assert err_gpu <= 1.5 * err_emul + 1e-3, f"GPU {err_gpu:.4g} vs bf16 emulation {err_emul:.4g} from fp64"
 
 
 def _oracle_margins(w, prompt, n):
-    """Oracle greedy stream plus the top-1 / top-2 logit margin at every step."""
+    """bf16-path oracle greedy stream plus the top-1 / top-2 logit margin at every step."""
     kv = O.Kv(w.shape)
-    logits, nk, nv, _ = O.full_forward(w, kv, prompt, keep_scores=False)
+    logits, nk, nv, _ = O.full_forward(w, kv, prompt, keep_scores=False, bf16=True)
     kv.push(nk, nv)
     rows = [logits[-1]]
     out = [O.argmax_first(rows[-1])]
     while len(out) < n:
-        logits, nk, nv, _ = O.full_forward(w, kv, [out[-1]], keep_scores=False)
+        logits, nk, nv, _ = O.full_forward(w, kv, [out[-1]], keep_scores=False, bf16=True)
         kv.push(nk, nv)
         rows.append(logits[0])
         out.append(O.argmax_first(rows[-1]))

@@ -493,7 +493,8 @@ def test_model_planted_mass_is_exactly_zero_elsewhere():      # test_model.py:18
             p = _np(p)
             cold = [j for j in range(p.shape[1]) if j not in planted]
             assert np.all(p[:, cold] == 0.0)
-            np.testing.assert_allclose(p.sum(axis=1), 1.0, atol=1e-9)
+            # the lse is the kernel's fp32 value (fp32 ulp at the +2000 bonus is 1.2e-4)
+            np.testing.assert_allclose(p.sum(axis=1), 1.0, atol=FP32_TOL)
     # the device accumulators (what the hot path uses) are exactly zero there too
     imp = _np(importance_from_log(log, len(cache) + 2))
     assert np.all(imp[[j for j in range(len(imp)) if j not in planted]] == 0.0)
@@ -648,7 +649,7 @@ def test_criterion_08_delayed_verification_stalls_exactly_once():  # test_accept
         kv = sd.KvPoolConfig(capacity_pages=1 << 20, page_bytes=64)
         reps = {}
         for mode in (sd.PipelineMode.DELAYED, sd.PipelineMode.SYNCHRONOUS):
-            cfg = sd.SimConfig(pipeline=mode, k=k, sparsity=0.2, max_batch=n)
+            cfg = sd.SimConfig(pipeline=mode, k=k, alpha=0.8, sparsity=0.2, max_batch=n)
             reps[mode] = sd.run_token_sim(wl, mc, cfg, kv)
         for r in reps[sd.PipelineMode.DELAYED].requests:
             assert r.stall_absences == r.rounds - 1, f"seed {seed} request {r.request_id}"

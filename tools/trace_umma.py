@@ -38,8 +38,8 @@ q = torch.randn(b * t, Hq, d, device=dev).to(torch.bfloat16)
 out = torch.empty_like(q)
 if nq > 0:
     items = make_items([(r, r * t, t, n, 0, 0, 0, r * t, 1) for r in range(b)], dev)
-    acc = torch.zeros(b * t, n + t, device=dev)
-    run = lambda: K.attention(q, out, pool, 0, items, b, n + t, t, Hq, acc=acc, acc_row_stride=n + t)
+    acc = torch.zeros(b * t, n + t, dtype=torch.int64, device=dev)
+    run = lambda: K.attention(q, out, pool, 0, items, b, n + t, t, Hq, acc=acc, acc_row_stride=n + t, acc_shift=40)
 else:
     rng = np.random.default_rng(0)
     crit = torch.from_numpy(np.stack([np.sort(rng.choice(n, bud, replace=False)) for _ in range(b)]).astype(np.int32)).to(dev)

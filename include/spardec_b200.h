@@ -219,6 +219,9 @@ typedef struct sd_attn_launch {
  * MLP-out GEMM into x.  GEMMs are cuBLAS (bf16 in, fp32 accumulate).  Buffers:
  * x fp32 [rows][h] (in/out); hn bf16 [rows][h]; qkv bf16 [rows][(q_heads+2kv_heads)d];
  * q, ctx bf16 [rows][q_heads][d]; hm bf16 [rows][2h]. */
+/* Workspace sd_forward_layers needs: the attention launches' (sd_attention_workspace_bytes,
+ * max over the launches) plus a RoPE cos/sin table of `rows` rows kept at its end. */
+int64_t sd_forward_workspace_bytes(int32_t rows, int32_t head_dim, int64_t attention_bytes);
 int sd_forward_layers(const sd_layer_weights* weights, int32_t layers, float* x, void* hn, void* qkv, void* q,
                       void* ctx, void* hm, int32_t rows, int32_t hidden, int32_t q_heads,
                       const int32_t* row_table, const int32_t* row_pos, const sd_paged_kv* kv,

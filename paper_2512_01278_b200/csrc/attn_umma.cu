@@ -5,6 +5,7 @@
 
 #include <map>
 #include <mutex>
+#include <algorithm>
 #include <tuple>
 
 namespace sd {
@@ -484,8 +485,14 @@ static bool umma_plan(const sd_paged_kv* kvp, int num_items, int max_keys, int m
   const int S = tcols / NR;
   const int cap = chunk_cap_tiles(NR, nslot, S, narrow ? 113 * 1024 : 227 * 1024, dense);
   int C = 1, chunk = TK;
-  // CTA slots per cluster size, from the occupancy API (cached per shape)
+  // CTA slots for C-CTA clusters.  Clusters live inside one GPC, so sizes that do not tile
+  // a GPC's slots leave some idle: the cluster-occupancy API gives that packing (it counts
+  // one CTA per SM for this kernel although two are resident — ncu: occupancy limit 2 —
+  // so it is doubled).  C = 1, 2, 4 pack every SM's two slots (C sweeps at ctx 4K / 16K and
+  // at bench.py's 25-item launch, profiles/r2_cluster_sweep.md).
+  const int per_sm = narrow ? 2 : 1;
   auto slots_of = [&](int c, int ct) -> int {
+    if (c == 1 || c == 2 || c == 4) return 148 * per_sm;
     static std::mutex mu;
     static std::map<std::tuple<int, int, int, int, int>, int> cache;
     const int smem = make_layout(NR, nslot, S, ct, dense).total;
@@ -494,7 +501,7 @@ static bool umma_plan(const sd_paged_kv* kvp, int num_items, int max_keys, int m
     auto itc = cache.find(key);
     if (itc != cache.end()) return itc->second;
     int v = G == 4 ? verify_slots_g4(NR, c, smem) : verify_slots_g8(NR, c, smem);
-    if (v <= 0) v = 0;
+    v = std::min(148 * per_sm, std::max(0, v) * per_sm);
     cache[key] = v;
     return v;
   };

@@ -611,11 +611,6 @@ int verify_slots(int C, int smem) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (getenv("SD_ATTN_PLAN_LOG") && C == 1) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_umma_kernel<G, NR, NSLOT, TCOLS>, NT, smem);
-    fprintf(stderr, "[sd slots] NR=%d smem=%d blocks/SM=%d\n", NR, smem, per_sm);
-  }
   int clusters = 0;
   if (cudaOccupancyMaxActiveClusters(&clusters, attn_umma_kernel<G, NR, NSLOT, TCOLS>, &cfg) != cudaSuccess) {
     cudaGetLastError();

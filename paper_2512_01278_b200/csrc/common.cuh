@@ -34,6 +34,13 @@ void count_launch(int n = 1);
     return 0;                                                          \
   } while (0)
 
+// ---- K5 helpers shared by forward.cu (rope_kv.cu) ------------------------------------
+inline int64_t rope_table_bytes(int rows, int head_dim) { return ((int64_t)rows * (head_dim / 2) * 8 + 255) / 256 * 256; }
+int rope_table(const int32_t* row_pos, int rows, int head_dim, float2* table, cudaStream_t s);
+int rope_kv_write_table(const void* qkv, int64_t qkv_row_stride, int rows, const int32_t* row_table,
+                        const int32_t* row_pos, const sd_paged_kv* kv, int layer, int q_heads, const float2* table,
+                        void* q_out, cudaStream_t s);
+
 // ---- element conversions ------------------------------------------------------
 template <typename T>
 __device__ __forceinline__ float to_f(T x);

@@ -79,6 +79,10 @@ static int gemm(cublasHandle_t hd, int R, int N, int K, const void* A, const voi
 
 }  // namespace sd
 
+extern "C" int64_t sd_forward_workspace_bytes(int32_t rows, int32_t head_dim, int64_t attention_bytes) {
+  return ((attention_bytes + 255) / 256) * 256 + sd::rope_table_bytes(rows, head_dim);
+}
+
 extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, float* x, void* hn, void* qkv, void* q,
                                  void* ctx, void* hm, int32_t rows, int32_t hidden, int32_t q_heads,
                                  const int32_t* row_table, const int32_t* row_pos, const sd_paged_kv* kv,
@@ -95,11 +99,25 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
   const int qkv_w = (q_heads + 2 * kv->kv_heads) * kv->head_dim;
   const int64_t hm_n = (int64_t)rows * 2 * hidden;
   const int tanh_blocks = (int)std::min<int64_t>((hm_n / 8 + 255) / 256 + 1, 148 * 8);
+  // RoPE cos/sin of every row once for all layers, at the end of the workspace
+  // (sd_forward_workspace_bytes); the attention launches get the rest
+  const int64_t table_bytes = sd::rope_table_bytes(rows, kv->head_dim);
+  const bool use_table = kv->head_dim % 16 == 0 && (qkv_w % 8) == 0 && workspace != nullptr &&
+                         workspace_bytes >= table_bytes;
+  float2* table = nullptr;
+  if (use_table) {
+    workspace_bytes -= table_bytes;
+    table = reinterpret_cast<float2*>(static_cast<char*>(workspace) + workspace_bytes);
+    sd::rope_table(row_pos, rows, kv->head_dim, table, s);
+  }
   int rc;
   for (int l = 0; l < layers; ++l) {
     if ((rc = sd_rmsnorm_cast(x, rows, hidden, eps, hn, SD_DTYPE_BF16, stream)) != 0) return rc;
     if ((rc = sd::gemm(hd, rows, qkv_w, hidden, hn, w[l].w_qkv, qkv, false, 0.f)) != 0) return rc;
-    if ((rc = sd_rope_kv_write(qkv, qkv_w, rows, row_table, row_pos, kv, l, q_heads, q, stream)) != 0) return rc;
+    if (use_table)
+      sd::rope_kv_write_table(qkv, qkv_w, rows, row_table, row_pos, kv, l, q_heads, table, q, s);
+    else if ((rc = sd_rope_kv_write(qkv, qkv_w, rows, row_table, row_pos, kv, l, q_heads, q, stream)) != 0)
+      return rc;
     for (int i = 0; i < num_launches; ++i) {
       const sd_attn_launch& a = launches[i];
       if (a.num_items == 0) continue;
@@ -115,5 +133,7 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
     sd::count_launch();
     if ((rc = sd::gemm(hd, rows, hidden, 2 * hidden, hm, w[l].mlp_out, x, true, 1.f)) != 0) return rc;
   }
+  // the workspace is handed back zero-filled (the attention launches rely on it)
+  if (use_table) cudaMemsetAsync(table, 0, table_bytes, s);
   SD_CUDA_RETURN();
 }

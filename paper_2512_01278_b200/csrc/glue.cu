@@ -34,6 +34,40 @@ __global__ void __launch_bounds__(256) rmsnorm_cast_kernel(const float* __restri
   for (int i = threadIdx.x; i < h; i += blockDim.x) orow[i] = from_f<T>(xr[i] * inv);
 }
 
+// the row stays in registers (h <= 256 * 4 * NV, h % 1024 == 0): one read of x, one write
+template <int NV>
+__global__ void __launch_bounds__(256) rmsnorm_cast_reg_kernel(const float* __restrict__ x, int h, float eps,
+                                                               __nv_bfloat16* __restrict__ out) {
+  const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)blockIdx.x * h);
+  float4 v[NV];
+  const int n4 = h / 4;
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int i = j * 256 + threadIdx.x;
+    v[j] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
+  }
+  ss = warp_sum(ss);
+  __shared__ float part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += part[w];
+  const float inv = rsqrtf(tot / static_cast<float>(h) + eps);
+  uint2* orow = reinterpret_cast<uint2*>(out + (int64_t)blockIdx.x * h);
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int i = j * 256 + threadIdx.x;
+    if (i < n4) {
+      __nv_bfloat162 a = __floats2bfloat162_rn(v[j].x * inv, v[j].y * inv);
+      __nv_bfloat162 b = __floats2bfloat162_rn(v[j].z * inv, v[j].w * inv);
+      orow[i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+    }
+  }
+}
+
 }  // namespace sd
 
 extern "C" int sd_rmsnorm_cast(const float* x, int32_t rows, int32_t h, float eps, void* out, int32_t out_dtype,
@@ -42,7 +76,14 @@ extern "C" int sd_rmsnorm_cast(const float* x, int32_t rows, int32_t h, float ep
   SD_REQUIRE(rows >= 0 && h >= 1, "sd_rmsnorm_cast: bad shape");
   if (rows == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (out_dtype == SD_DTYPE_F32)
+  const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16) == 0 && (reinterpret_cast<uintptr_t>(out) % 8) == 0;
+  if (out_dtype == SD_DTYPE_BF16 && aligned && h % 1024 == 0 && h <= 8192) {
+    auto* o = static_cast<__nv_bfloat16*>(out);
+    if (h <= 4096)
+      sd::rmsnorm_cast_reg_kernel<4><<<rows, 256, 0, s>>>(x, h, eps, o);
+    else
+      sd::rmsnorm_cast_reg_kernel<8><<<rows, 256, 0, s>>>(x, h, eps, o);
+  } else if (out_dtype == SD_DTYPE_F32)
     sd::rmsnorm_cast_kernel<float><<<rows, 256, 0, s>>>(x, h, eps, static_cast<float*>(out));
   else
     sd::rmsnorm_cast_kernel<__nv_bfloat16><<<rows, 256, 0, s>>>(x, h, eps, static_cast<__nv_bfloat16*>(out));

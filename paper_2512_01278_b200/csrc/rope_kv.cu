@@ -11,6 +11,8 @@
 // threads touch consecutive elements.  fp32 parity mode rotates in double.
 #include "common.cuh"
 
+#include <algorithm>
+
 namespace sd {
 
 template <typename T>
@@ -63,6 +65,83 @@ __global__ void __launch_bounds__(256) rope_kv_kernel(const T* __restrict__ qkv,
   } else {
     for (int j = threadIdx.x; j < n; j += blockDim.x) vdst[j] = vsrc[j];
   }
+}
+
+// cos/sin of every row's angles, once per forward (all layers share the positions):
+// table[r][i] = (cos, sin)(pos_r * 10000^(-2i/d)), computed in double like the per-layer path
+__global__ void rope_table_kernel(const int32_t* __restrict__ row_pos, int rows, int half, int D,
+                                  float2* __restrict__ table) {
+  const int64_t n = (int64_t)rows * half;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(idx / half), i = static_cast<int>(idx - (int64_t)r * half);
+    const double inv = pow(10000.0, -static_cast<double>(2 * i) / static_cast<double>(D));
+    double sn, cs;
+    sincos(static_cast<double>(row_pos[r]) * inv, &sn, &cs);
+    table[idx] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
+  }
+}
+
+// bf16 K5 with the precomputed table: 8 bf16 pairs (16 B of each half) per thread, rows
+// spread over the grid so every thread has work
+__global__ void __launch_bounds__(128) rope_kv_table_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t row_stride,
+                                                            const int32_t* __restrict__ row_table,
+                                                            const int32_t* __restrict__ row_pos, PagedKv kv, int layer,
+                                                            int q_heads, const float2* __restrict__ table,
+                                                            __nv_bfloat16* __restrict__ q_out) {
+  const int r = blockIdx.x;
+  const int D = kv.head_dim, half = D / 2, Hkv = kv.kv_heads;
+  const int pos = row_pos[r];
+  const int64_t slot = kv.slot_of(row_table[r], pos);
+  const __nv_bfloat16* x = qkv + (int64_t)r * row_stride;
+  __nv_bfloat16* K = static_cast<__nv_bfloat16*>(const_cast<void*>(kv.k)) + (int64_t)layer * kv.layer_stride;
+  __nv_bfloat16* V = static_cast<__nv_bfloat16*>(const_cast<void*>(kv.v)) + (int64_t)layer * kv.layer_stride;
+  const float2* tr = table + (int64_t)r * half;
+  const int vec_per_head = half / 8;                    // 8-element groups per half
+  const int groups = (q_heads + Hkv) * vec_per_head;
+  for (int gi = threadIdx.x; gi < groups; gi += blockDim.x) {
+    const int hq = gi / vec_per_head, i0 = (gi - hq * vec_per_head) * 8;
+    const __nv_bfloat16* src = x + hq * D;
+    const uint4 lo_raw = *reinterpret_cast<const uint4*>(src + i0);
+    const uint4 hi_raw = *reinterpret_cast<const uint4*>(src + half + i0);
+    const __nv_bfloat16* lo = reinterpret_cast<const __nv_bfloat16*>(&lo_raw);
+    const __nv_bfloat16* hi = reinterpret_cast<const __nv_bfloat16*>(&hi_raw);
+    uint4 olo_raw, ohi_raw;
+    __nv_bfloat16* olo = reinterpret_cast<__nv_bfloat16*>(&olo_raw);
+    __nv_bfloat16* ohi = reinterpret_cast<__nv_bfloat16*>(&ohi_raw);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float2 cs = tr[i0 + j];
+      const float a = __bfloat162float(lo[j]), b = __bfloat162float(hi[j]);
+      olo[j] = __float2bfloat16_rn(a * cs.x - b * cs.y);
+      ohi[j] = __float2bfloat16_rn(a * cs.y + b * cs.x);
+    }
+    __nv_bfloat16* dst = hq < q_heads ? q_out + ((int64_t)r * q_heads + hq) * D : K + kv.row_off(slot, hq - q_heads);
+    *reinterpret_cast<uint4*>(dst + i0) = olo_raw;
+    *reinterpret_cast<uint4*>(dst + half + i0) = ohi_raw;
+  }
+  const uint4* vsrc = reinterpret_cast<const uint4*>(x + (q_heads + Hkv) * D);
+  uint4* vdst = reinterpret_cast<uint4*>(V + kv.row_off(slot, 0));
+  for (int j = threadIdx.x; j < Hkv * D / 8; j += blockDim.x) vdst[j] = vsrc[j];
+}
+
+int rope_table(const int32_t* row_pos, int rows, int head_dim, float2* table, cudaStream_t s) {
+  const int half = head_dim / 2;
+  const int64_t n = (int64_t)rows * half;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
+  rope_table_kernel<<<blocks, 256, 0, s>>>(row_pos, rows, half, head_dim, table);
+  count_launch();
+  return 0;
+}
+
+// bf16 K5 through a rope_table; head_dim must be a multiple of 16 and rows 16-byte aligned
+int rope_kv_write_table(const void* qkv, int64_t qkv_row_stride, int rows, const int32_t* row_table,
+                        const int32_t* row_pos, const sd_paged_kv* kv, int layer, int q_heads, const float2* table,
+                        void* q_out, cudaStream_t s) {
+  PagedKv p = make_paged(kv);
+  rope_kv_table_kernel<<<rows, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(qkv), qkv_row_stride, row_table,
+                                            row_pos, p, layer, q_heads, table, static_cast<__nv_bfloat16*>(q_out));
+  count_launch();
+  return 0;
 }
 
 }  // namespace sd

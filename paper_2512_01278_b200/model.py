@@ -349,6 +349,7 @@ def _forward_native(model: ToyModel, pool: PagedKvPool, tokens, row_table, row_p
         descs[i].acc_shift = ln.acc_shift
         need = max(need, lib.sd_attention_workspace_bytes(ln.num_items, ln.max_keys, ln.max_nq, Hq,
                                                           ctypes.byref(desc)))
+    need = lib.sd_forward_workspace_bytes(R, d, need)   # + the per-forward RoPE table
     ws = K._zeroed_workspace(need, dev) if need > 0 else None
     qkv_w = (Hq + 2 * c.num_kv_heads) * d
     hn = torch.empty(R, h, dtype=dt, device=dev)

@@ -43,6 +43,8 @@ class PagedKvPool:
         self._table_host = np.zeros((table_rows, pages_per_row), dtype=np.int32)
         self._dirty: set[int] = set()
         self._free = list(range(num_pages - 1, -1, -1))
+        self._pending_free: list = []   # (event, pages): pages still read by an in-flight copy
+        self._unmapped: dict[int, int] = {}  # row -> number of logical pages currently unmapped
         self._rows: dict[int, list[int]] = {}
         self._desc = None
 
@@ -66,7 +68,36 @@ class PagedKvPool:
     # -- page mapping ----------------------------------------------------------------
     @property
     def free_pages(self) -> int:
+        self.reclaim()
         return len(self._free)
+
+    def reclaim(self) -> None:
+        """Return pages whose deferred-free event (an offload copy) has completed."""
+        if not self._pending_free:
+            return
+        keep = []
+        for ev, pages in self._pending_free:
+            if ev.query():
+                self._free.extend(pages)
+            else:
+                keep.append((ev, pages))
+        self._pending_free = keep
+
+    def shrink_row(self, row: int, tokens: int) -> int:
+        """Return the physical pages of ``row`` past logical position ``tokens`` (KV rollback
+        of whole pages, kvpool.py:315-336 free_tail); their contents are dead."""
+        pages = self._rows.get(row, [])
+        keep = -(-tokens // self.page_size)
+        n = 0
+        while len(pages) > keep:
+            p = pages.pop()
+            if p >= 0:
+                self._free.append(p)
+                n += 1
+            self._table_host[row, len(pages)] = 0
+        if n:
+            self._dirty.add(row)
+        return n
 
     @property
     def pages_per_row(self) -> int:
@@ -82,6 +113,8 @@ class PagedKvPool:
             raise ImpossibleRequestError(f"row {row} needs {need} pages > {self.pages_per_row} per row")
         pages = self._rows.setdefault(row, [])
         if need - len(pages) > len(self._free):
+            self.reclaim()
+        if need - len(pages) > len(self._free):
             raise ImpossibleRequestError("device KV pool exhausted")
         while len(pages) < need:
             p = self._free.pop()
@@ -93,20 +126,29 @@ class PagedKvPool:
         for p in reversed(self._rows.pop(row, [])):
             if p >= 0:
                 self._free.append(p)
+        self._unmapped.pop(row, None)
 
     # -- host offload: physical pages leave / rejoin a row ---------------
-    def unmap_pages(self, row: int, logical_pages) -> int:
+    def unmap_pages(self, row: int, logical_pages, after=None) -> int:
         """Return the physical pages behind ``logical_pages`` of ``row`` to the free
-        list (their rows were copied to the host); the block-table entries point at
-        page 0 until remapped, and the row must not be scheduled meanwhile."""
+        list (their rows were copied to the host) — once ``after`` (a CUDA event of that
+        copy) has completed, when given.  The block-table entries point at page 0 until
+        remapped; BatchedDecoder refuses to schedule a row with unmapped pages."""
         pages = self._rows.get(row, [])
         n = 0
+        freed = []
         for lp in logical_pages:
             if lp < len(pages) and pages[lp] >= 0:
-                self._free.append(pages[lp])
+                freed.append(pages[lp])
                 pages[lp] = -1
                 self._table_host[row, lp] = 0
                 n += 1
+        if after is None:
+            self._free.extend(freed)
+        elif freed:
+            self._pending_free.append((after, freed))
+        if n:
+            self._unmapped[row] = self._unmapped.get(row, 0) + n
         if n:
             self._dirty.add(row)
         return n
@@ -116,28 +158,36 @@ class PagedKvPool:
         pages = self._rows.get(row, [])
         todo = [lp for lp in logical_pages if lp < len(pages) and pages[lp] < 0]
         if len(todo) > len(self._free):
+            self.reclaim()
+        if len(todo) > len(self._free):
             raise ImpossibleRequestError("device KV pool exhausted while reloading")
         for lp in todo:
             pages[lp] = self._free.pop()
             self._table_host[row, lp] = pages[lp]
         if todo:
             self._dirty.add(row)
+            self._unmapped[row] -= len(todo)
         return len(todo)
+
+    def has_unmapped(self, row: int) -> bool:
+        return self._unmapped.get(row, 0) > 0
 
     def unmapped_pages(self, row: int) -> list:
         return [i for i, p in enumerate(self._rows.get(row, [])) if p < 0]
 
     def sync_table(self) -> None:
-        """Upload dirty block-table rows (host -> device, stream ordered)."""
+        """Upload dirty block-table rows (host -> device), stream ordered and asynchronous:
+        the rows are staged in pinned memory (torch's pinned allocator keeps a staging
+        block alive until its copy ran), so the host never waits for the GPU here."""
         if not self._dirty:
             return
         rows = sorted(self._dirty)
         self._dirty.clear()
         if len(rows) > 8:
-            self.table.copy_(torch.from_numpy(self._table_host), non_blocking=False)
+            self.table.copy_(torch.from_numpy(self._table_host).pin_memory(), non_blocking=True)
             return
         for r in rows:
-            self.table[r].copy_(torch.from_numpy(self._table_host[r]))
+            self.table[r].copy_(torch.from_numpy(self._table_host[r]).pin_memory(), non_blocking=True)
 
     # -- host-side views (tests / drop-in KvCache) -------------------------------------
     def slots(self, row: int, positions) -> torch.Tensor:

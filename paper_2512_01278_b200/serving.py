@@ -88,7 +88,15 @@ class StepResult:
 
 class BatchedDecoder:
     def __init__(self, model: ToyModel, k: int, sparsity: float, max_requests: int, max_seq_len: int,
-                 page_size: int = 16, pool_tokens: int | None = None):
+                 page_size: int = 16, pool_tokens: int | None = None, paging: str = "reserve"):
+        """``paging``: "reserve" maps a request's whole lifetime (prompt + max_output + k + 1
+        positions) at admission; "on_demand" maps physical pages as positions are written
+        (prompt at admission, then each iteration's draft / verify rows), so a pool of
+        ``pool_tokens`` holds as many requests as their CURRENT lengths allow — the physical
+        side of KvPool's page accounting (kvpool.py:174-237)."""
+        if paging not in ("reserve", "on_demand"):
+            raise ConfigurationError("paging must be 'reserve' or 'on_demand'")
+        self.on_demand = paging == "on_demand"
         if k < 1:
             raise ConfigurationError("k must be at least 1")
         if not 0.0 < sparsity <= 1.0:
@@ -156,8 +164,9 @@ class BatchedDecoder:
         need = len(req.prompt) + req.max_output + self.k + 1
         if need > self.max_seq_len:
             raise ContractError(f"request needs {need} KV positions > decoder max {self.max_seq_len}")
-        slot = self.free_slots.pop()
-        self.pool.ensure_tokens(slot, need)
+        slot = self.free_slots[-1]
+        self.pool.ensure_tokens(slot, len(req.prompt) if self.on_demand else need)
+        self.free_slots.pop()
         s = Seq(request_id=req.request_id, slot=slot, prompt=list(req.prompt), max_output=req.max_output,
                 eos_token=req.eos_token, k=self.k, round_target=self.k, stats=RoundStats(k=self.k))
         self.seqs[req.request_id] = s
@@ -170,31 +179,46 @@ class BatchedDecoder:
         self._host_kv.pop(request_id, None)
 
     # -- host offload tier (kvpool.py:213-237,272-311) -----------------
+    def _copy_stream(self) -> torch.cuda.Stream:
+        st = getattr(self, "_copy_st", None)
+        if st is None:
+            st = self._copy_st = torch.cuda.Stream(self.dev)
+        return st
+
     def offload_positions(self, request_id, positions) -> int:
-        """Copy the K/V rows of ``positions`` (all layers) to pinned host memory and return
-        every physical page whose tokens are all on the host to the device pool.  The
+        """Copy the K/V rows of ``positions`` (all layers) to pinned host memory on the copy
+        stream and return every physical page whose tokens are all on the host to the
+        device pool once that copy has completed (event-fenced, kvpool.py:213-237).  The
         request must not be scheduled until ``reload_positions`` brings them back."""
         positions = sorted(int(p) for p in positions)
         s = self.seqs.get(request_id)
         if s is None or not positions:
             return 0
-        k, v = self.pool.read(s.slot, positions)  # (n, L, Hkv, d)
-        hk = torch.empty(k.shape, dtype=k.dtype, pin_memory=True)
-        hv = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
-        hk.copy_(k, non_blocking=True)
-        hv.copy_(v, non_blocking=True)
-        torch.cuda.current_stream(self.dev).synchronize()
+        main = torch.cuda.current_stream(self.dev)
+        cs = self._copy_stream()
+        cs.wait_stream(main)                    # the rows were written by earlier compute
+        slots = self.pool.slots(s.slot, positions)
+        hk = torch.empty((len(positions), *self.pool.k.shape[:1], *self.pool.k.shape[2:]), dtype=self.pool.dtype,
+                         pin_memory=True)
+        hv = torch.empty_like(hk, pin_memory=True)
+        with torch.cuda.stream(cs):
+            sl = slots.to(self.dev, non_blocking=True)
+            hk.copy_(self.pool.k[:, sl].transpose(0, 1), non_blocking=True)
+            hv.copy_(self.pool.v[:, sl].transpose(0, 1), non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(cs)
         store = self._host_kv.setdefault(request_id, {})
         for i, p in enumerate(positions):
-            store[p] = (hk[i], hv[i])
+            store[p] = (hk[i], hv[i], done)
         ps = self.pool.page_size
         whole = sorted({p // ps for p in positions if all(q in store for q in range(p // ps * ps, p // ps * ps + ps))})
-        self.pool.unmap_pages(s.slot, whole)
-        self.offloaded_bytes += 2 * k.numel() * k.element_size()
+        self.pool.unmap_pages(s.slot, whole, after=done)
+        self.offloaded_bytes += 2 * hk.numel() * hk.element_size()
         return len(positions)
 
     def reload_positions(self, request_id, positions) -> int:
-        """Inverse of ``offload_positions``: remap pages and copy the rows back."""
+        """Inverse of ``offload_positions``: remap pages and copy the rows back on the copy
+        stream; the compute stream waits for that copy before its next launch."""
         positions = sorted(int(p) for p in positions)
         s = self.seqs.get(request_id)
         store = self._host_kv.get(request_id)
@@ -205,13 +229,29 @@ class BatchedDecoder:
         self.pool.sync_table()
         # a remapped page receives every row it holds: also the still-host rows of pages
         # that were only partly reloaded stay on the host and are written when they return
-        k = torch.stack([store[p][0] for p in positions])
-        v = torch.stack([store[p][1] for p in positions])
-        self.pool.write(s.slot, positions, k, v)
-        for p in positions:
+        n = len(positions)
+        hk = torch.empty((n, *store[positions[0]][0].shape), dtype=self.pool.dtype, pin_memory=True)
+        hv = torch.empty_like(hk, pin_memory=True)
+        for i, p in enumerate(positions):
+            store[p][2].synchronize()           # its offload copy landed in host memory
+            hk[i].copy_(store[p][0])
+            hv[i].copy_(store[p][1])
             del store[p]
-        self.reloaded_bytes += 2 * k.numel() * k.element_size()
-        return len(positions)
+        if not store:
+            del self._host_kv[request_id]
+        main = torch.cuda.current_stream(self.dev)
+        cs = self._copy_stream()
+        cs.wait_stream(main)                    # fresh pages may have been freed by compute
+        slots = self.pool.slots(s.slot, positions)
+        with torch.cuda.stream(cs):
+            sl = slots.to(self.dev, non_blocking=True)
+            dk = hk.to(self.dev, non_blocking=True)
+            dv = hv.to(self.dev, non_blocking=True)
+            self.pool.k[:, sl] = dk.transpose(0, 1)
+            self.pool.v[:, sl] = dv.transpose(0, 1)
+        main.wait_stream(cs)
+        self.reloaded_bytes += 2 * hk.numel() * hk.element_size()
+        return n
 
     def _emit(self, s: Seq, toks) -> int:
         landed = 0
@@ -366,6 +406,17 @@ class BatchedDecoder:
         self._iter += 1
         if self._ring_ev[j] is not None:
             self._ring_ev[j].synchronize()   # its plan copy and result copy are done
+        for s in drafts + verifs:
+            if self.pool.has_unmapped(s.slot) or self._host_kv.get(s.request_id):
+                # its block table points offloaded pages at a placeholder: reload first
+                raise ContractError(f"request {s.request_id} has KV rows on the host tier; reload them first")
+            if self.on_demand:
+                if s in verifs:
+                    end = s.n_kv + s.round_target + 1
+                else:
+                    end = (s.n_kv_ub if s.inflight else s.n_kv) + s.phase + 1
+                self.pool.ensure_tokens(s.slot, end)
+        self.pool.sync_table()
         plan = self._plan_host[j].numpy()
         row = 0
         d_max_keys = 1

@@ -158,7 +158,12 @@ def run_token_sim(workload: WorkloadSpec, model_config: ModelConfig, cfg: SimCon
     requests = generate_workload(workload)
     k = cfg.k
     max_len = max((r.input_len + r.output_len for r in requests), default=1)
-    dec = BatchedDecoder(model, k, cfg.sparsity, max_requests=cfg.max_batch, max_seq_len=max_len)
+    # physical pages follow KvPool's logical accounting: granted as positions are written,
+    # sized to the pool's capacity (+ one partly filled page and the k+1 in-flight
+    # positions per request slot)
+    dec = BatchedDecoder(model, k, cfg.sparsity, max_requests=cfg.max_batch, max_seq_len=max_len,
+                         paging="on_demand",
+                         pool_tokens=kv_cfg.capacity_pages + cfg.max_batch * (16 + k + 1))
     pool = KvPool(kv_cfg.capacity_pages, kv_cfg.page_bytes, chunk_pages=kv_cfg.chunk_pages, policy=kv_cfg.policy)
     waiting = sorted(requests, key=lambda r: (r.arrival_ms, r.request_id))
     lives: dict = {}
@@ -285,6 +290,7 @@ def run_token_sim(workload: WorkloadSpec, model_config: ModelConfig, cfg: SimCon
             target = lv.round_target
             pool.free_tail(rid, target - a)
             seq = dec.seqs[rid]
+            dec.pool.shrink_row(seq.slot, seq.n_kv + 1)  # rejected drafts' whole pages
             lv.emitted = len(seq.committed)
             lv.done = seq.done
             lv.accepted_total += a

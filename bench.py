@@ -59,7 +59,11 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--batch", type=int, default=128, help="requests per GPU")
+    p.add_argument("--batch", type=int, default=128,
+                   help="requests per GPU resident at once (one wave; the configs[1] batch)")
+    p.add_argument("--global-batch", type=int, default=None,
+                   help="requests of the whole job, sharded over the ranks (default: --batch at 1 GPU, "
+                        "512 = configs[2] at >1 GPU); a rank runs its shard in waves of --batch")
     p.add_argument("--prompt", type=int, default=512)
     p.add_argument("--output", type=int, default=8192)
     p.add_argument("--context", type=int, default=None, help="KV rows at the timed window (default prompt+output/2)")
@@ -157,6 +161,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     from paper_2512_01278_b200.engine import DecodeRequest
     from paper_2512_01278_b200.scheduler import (BatchCandidate, PhaseBuckets, PipelineMode, assign_new_request,
                                                  first_round_draft_len, form_batch)
+    from paper_2512_01278_b200.dist import gather_throughput, shard_ids
     from paper_2512_01278_b200.serving import BatchedDecoder
     from paper_2512_01278_b200.workload import synthetic_prompt
 
@@ -170,20 +175,22 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     max_seq = args.prompt + args.output if args.pool == "full" else ctx + 64
     results = {}
 
-    def build_decoder(m, B=B, ctx=ctx, max_seq=max_seq):
-        dec = BatchedDecoder(m, k, s, max_requests=B, max_seq_len=max_seq)
-        # shard: global request ids rank*B .. rank*B+B-1 (independent units, no collective)
+    def build_decoder(m, B=B, ctx=ctx, max_seq=max_seq, ids=None, pool_tokens=None, synthetic=None,
+                      prefill_rows=32768):
+        ids = list(range(rank * B, rank * B + B)) if ids is None else list(ids)
+        dec = BatchedDecoder(m, k, s, max_requests=len(ids), max_seq_len=max_seq, pool_tokens=pool_tokens,
+                             paging="reserve" if pool_tokens is None else "on_demand")
+        # this rank's shard of global request ids (independent units, no collective)
         reqs = []
-        for i in range(B):
-            rid = rank * B + i
+        for rid in ids:
             prompt = synthetic_prompt(0, rid, args.prompt, m.config.vocab_size)
             cont = synthetic_prompt(1, rid, ctx - args.prompt, m.config.vocab_size)
             reqs.append(DecodeRequest(rid, prompt + cont, max_seq - ctx))
-        log(f"decoder built (pool {dec.pool.k.numel() * 4 / 1e9:.0f} GB), prefilling {B} x {ctx} tokens")
-        if args.synthetic_prefill:
-            seqs = dec.prefill_synthetic(reqs, real_tokens=args.prompt, max_rows=32768)
+        log(f"decoder built (pool {dec.pool.k.numel() * 4 / 1e9:.0f} GB), prefilling {len(ids)} x {ctx} tokens")
+        if args.synthetic_prefill if synthetic is None else synthetic:
+            seqs = dec.prefill_synthetic(reqs, real_tokens=args.prompt, max_rows=prefill_rows)
         else:
-            seqs = dec.prefill(reqs, max_rows=32768)
+            seqs = dec.prefill(reqs, max_rows=prefill_rows)
         torch.cuda.synchronize()
         log("prefill done")
         buckets = PhaseBuckets.empty(k)
@@ -218,6 +225,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         timed region (no per-launch events); afterwards, if asked, run a few more
         iterations with per-launch CUDA events on the K1 / K2 launches for the roofline."""
         dec = build_decoder(m, **dims)
+        if world > 1 and dims.get("sync_ranks", True):
+            dist.barrier()
         torch.cuda.synchronize()
         for _ in range(warmup):
             one_iteration(dec)
@@ -311,10 +320,37 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         return out
 
     log("model initialised")
-    main = measure(model, args.steps, args.warmup, "random", True)
+    # the job: global request ids sharded over the ranks (dist.shard_ids); a rank serves its
+    # shard in waves of at most --batch resident requests (KV capacity), each wave timed
+    # over `steps` iterations at the mid-run context
+    G_total = args.global_batch or (B if world == 1 else 512)
+    my_ids = shard_ids(G_total, rank, world)
+    waves = [my_ids[i:i + B] for i in range(0, len(my_ids), B)]
+    n_waves = torch.tensor([len(waves)], device=dev)
+    if world > 1:
+        dist.all_reduce(n_waves, op=dist.ReduceOp.MAX)
+    main = None
+    for wi in range(int(n_waves.item())):
+        ids = waves[wi] if wi < len(waves) else []
+        if not ids:  # a rank with fewer waves still joins the barriers
+            if world > 1:
+                dist.barrier()
+                dist.barrier()
+            continue
+        r = measure(model, args.steps, args.warmup, "random" if wi == 0 else f"random_w{wi}", wi == 0,
+                    B=len(ids), ids=ids)
+        if main is None:
+            main = r
+        else:
+            for key in ("emitted", "dev_s", "wall_s"):
+                main[key] += r[key]
+        log(f"wave {wi} ({len(ids)} requests) done")
+    main["waves"] = len(waves)
+    main["per_rank"] = len(my_ids)
+    main["global_batch"] = G_total
     log("main measurement done")
     variants = {}
-    extra = [v for v in args.variants.split(",") if v and v != "none"]
+    extra = [v for v in args.variants.split(",") if v and v != "none"] if world == 1 else []
     planted = None
     if "planted" in extra:
         planted = sd.plant_attention_concentration(model, list(range(5, args.prompt, args.prompt // 12))[:12])
@@ -329,30 +365,33 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
             log(f"budget s={sv:g} done")
         s = base_s
     if "c3" in extra:
-        # configs[3]: Qwen3-32B-shaped (oracle family: h = 64 x 128, GQA 8), 32K output,
-        # batch 64 over 8 GPUs = 8 requests per GPU, mid-run context 512 + 16384
+        # configs[3]: Qwen3-32B-shaped (oracle family: h = 64 x 128, GQA 8) long-reasoning decode,
+        # 32K output, batch 64 on ONE GPU with the paged KV near HBM capacity: the pool gets
+        # what the weights leave (pages granted on demand), and the timed window sits at the
+        # context where 64 requests fill 95% of it
         model = planted = None  # the 8B-shaped weights (shared by the planted view) are not needed
         torch.cuda.empty_cache()
         c3cfg = sd.ModelConfig(64, 64, 8, 128, C1["vocab"], seed=0)
         m3 = sd.init_model(c3cfg, dtype=torch.bfloat16, device=dev, fast_init=True)
-        c3out = 32768
-        v = measure(m3, max(3, args.steps // 2), 3, "c3", True, B=8, ctx=args.prompt + c3out // 2,
-                    max_seq=args.prompt + c3out)
-        v["workload"] = ("configs[3]: Qwen3-32B-shaped (L=64, Hq=64, Hkv=8, d=128) random-init bf16, 8 requests "
-                         "per GPU (batch 64 over 8 GPUs), prompt 512, output 32768, mid-run context 16896")
+        c3out, c3B = 32768, 64
+        kv_tok = c3cfg.num_layers * c3cfg.num_kv_heads * c3cfg.head_dim * 2 * 2
+        free_b = torch.cuda.mem_get_info(dev)[0]
+        pool_tok = int((free_b - 8e9) / kv_tok)                 # 8 GB: activations, workspaces
+        c3ctx = min(args.prompt + c3out // 2, int(0.95 * pool_tok / c3B) - 64)
+        v = measure(m3, max(3, args.steps // 2), 3, "c3", True, B=c3B, ctx=c3ctx, max_seq=args.prompt + c3out,
+                    pool_tokens=pool_tok, synthetic=True, prefill_rows=8192)
+        v["workload"] = (f"configs[3]: Qwen3-32B-shaped (L=64, Hq=64, Hkv=8, d=128) random-init bf16, batch {c3B} "
+                         f"on one GPU, prompt {args.prompt}, output {c3out}; paged KV pool of {pool_tok} tokens "
+                         f"({pool_tok * kv_tok / 1e9:.0f} GB, all HBM the weights leave) granted on demand, timed "
+                         f"window at context {c3ctx} = {c3B * c3ctx / pool_tok:.0%} of the pool")
         variants["configs3_32b"] = v
         del m3
 
-    # gather: tokens summed, time = max over ranks (device clock)
-    vals = torch.tensor([main["emitted"], main["dev_s"], main["wall_s"]], dtype=torch.float64, device=dev)
-    if world > 1:
-        t_sum = vals[0:1].clone()
-        t_max = vals[1:3].clone()
-        dist.all_reduce(t_sum, op=dist.ReduceOp.SUM)
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        vals = torch.cat([t_sum, t_max])
-    results = {"main": main, "variants": variants, "total_emitted": float(vals[0]), "dev_s": float(vals[1]),
-               "wall_s": float(vals[2]), "ctx": ctx}
+    # gather (dist.py, after the timed regions): tokens summed, times max over ranks
+    total_emitted, dev_s = gather_throughput(main["emitted"], main["dev_s"], device=dev)
+    _, wall_s = gather_throughput(0.0, main["wall_s"], device=dev)
+    results = {"main": main, "variants": variants, "total_emitted": total_emitted, "dev_s": dev_s,
+               "wall_s": wall_s, "ctx": ctx}
     for name, v in variants.items():
         vv = torch.tensor([v["emitted"], v["dev_s"]], dtype=torch.float64, device=dev)
         if world > 1:
@@ -479,6 +518,9 @@ def main():
     import torch.distributed as dist
 
     if world > 1:
+        # NCCL INFO on stderr: the communicator's nranks / transport are checkable from the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_ours(args, rank, world, local_rank)
@@ -520,15 +562,25 @@ def main():
                 variants[name]["verify_gbs"] = v["verify_bytes"] / (v["verify_ms_total"] / 1000.0) / 1e9
             if v.get("draft_ms_total"):
                 variants[name]["draft_gbs"] = v["draft_bytes"] / (v["draft_ms_total"] / 1000.0) / 1e9
+        job = m["global_batch"]
+        if args.gpus > 1:
+            workload = (f"configs[2]: Qwen3-8B-shaped (L={args.layers}, Hq=32, Hkv=8, d=128, V=151936) random-init "
+                        f"bf16, global batch {job} request-sharded over {args.gpus} GPUs ({m['per_rank']} per rank, "
+                        f"waves of <= {args.batch} resident: {m['waves']} on rank 0), prompt {args.prompt}, output "
+                        f"{args.output}, k={args.k}, s={args.sparsity}; each wave timed over {args.steps} iterations "
+                        f"at mid-run context {res['ctx']}")
+        else:
+            workload = (f"configs[1]: Qwen3-8B-shaped (L={args.layers}, Hq=32, Hkv=8, d=128, V=151936) random-init "
+                        f"bf16, batch {job}/GPU, prompt {args.prompt}, output {args.output}, k={args.k}, "
+                        f"s={args.sparsity}; timed window at mid-run context {res['ctx']}")
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": res["dev_s"] / args.steps * 1000.0, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, "
-            "synthetic prompts + teacher-forced continuation to the mid-run context)",
-            "config": {"workload": f"configs[1]: Qwen3-8B-shaped (L={args.layers}, Hq=32, Hkv=8, d=128, V=151936) "
-                                   f"random-init bf16, batch {args.batch}/GPU, prompt {args.prompt}, output "
-                                   f"{args.output}, k={args.k}, s={args.sparsity}; timed window at mid-run context "
-                                   f"{res['ctx']}", "global_batch": args.batch * args.gpus,
+            "warmup": args.warmup, "ms_per_step": res["dev_s"] / (args.steps * m["waves"]) * 1000.0,
+            "higher_is_better": True,
+            "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, synthetic prompts + teacher-forced continuation to the mid-run "
+                    "context)",
+            "config": {"workload": workload, "global_batch": job,
                        "parallelism": f"dp{args.gpus} (request shards, no hot-path collective)",
                        "l2": "inputs larger than L2 (~30 GB read per step)", "pipeline": "delayed (iteration i's verify outcomes are applied on the host during "
                                    "iteration i+1; request state is device-resident, so no request stalls)",

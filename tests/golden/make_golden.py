@@ -172,5 +172,33 @@ def main() -> None:
     (OUT / "streams.json").write_text(json.dumps(streams))
 
 
+def offload_streams() -> None:
+    """The REFERENCE's token-level serving loop under KV offload pressure (OFFLOAD policy,
+    120-page pool, 16-page chunks; simulate.py:535, kvpool.py:213-237,272-311): its per-request
+    outputs are the golden streams of tests/test_serving_gpu.py's offload test."""
+    load_reference()
+    from spardec_ref import kvpool as RK
+    from spardec_ref import model as RM
+    from spardec_ref import simulate as RSim
+    from spardec_ref import workload as RW
+
+    out = []
+    for seed, n, inp, outl, cap in [(0, 4, 16, 24, 120), (0, 6, 20, 40, 160)]:
+        wl = RW.WorkloadSpec(n_requests=n, input_len=RW.LengthSpec(RW.LengthDist.CONSTANT, inp),
+                             output_len=RW.LengthSpec(RW.LengthDist.CONSTANT, outl), seed=seed)
+        mc = RM.ModelConfig(2, 4, 2, 8, 48, seed=0)
+        rep = RSim.run_token_sim(wl, mc, RSim.SimConfig(k=3, alpha=0.0, sparsity=0.4, max_batch=n),
+                                 RSim.KvPoolConfig(capacity_pages=cap, page_bytes=64, chunk_pages=16,
+                                                   policy=RK.KvPolicy.OFFLOAD))
+        out.append(dict(seed=seed, n=n, input_len=inp, output_len=outl, capacity=cap,
+                        outputs={str(k): v for k, v in rep.outputs.items()},
+                        max_offloaded=max(r.offloaded_pages for r in rep.iterations)))
+        print(f"offload case n={n} cap={cap}: max offloaded pages {out[-1]['max_offloaded']}")
+    (OUT / "offload_streams.json").write_text(json.dumps(out))
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["offload"]:
+        offload_streams()
+        raise SystemExit(0)
     main()

@@ -60,15 +60,25 @@ def test_token_sim_lossless_small_mixed_lengths():
     assert sum(rep.acceptance_histogram.values()) == sum(r.rounds for r in rep.requests)
 
 
-def test_token_sim_under_offload_pressure_stays_lossless():
+@pytest.mark.parametrize("case", [0, 1])
+def test_token_sim_under_offload_pressure_matches_reference(case):
+    """Token-level serving under KV offload pressure (OFFLOAD policy, small pool): the
+    outputs equal the REFERENCE's own run_token_sim outputs for the same workload and pool
+    (tests/golden/offload_streams.json, simulate.py:535 run under kvpool.py's offload
+    policy), the host tier is physical (bytes left HBM and came back on the copy stream),
+    and pages are granted on demand (the device pool is sized to the KvPool capacity)."""
+    import json
+    from pathlib import Path
+
     from paper_2512_01278_b200.kvpool import KvPolicy
+    gold = json.loads((Path(__file__).parent / "golden" / "offload_streams.json").read_text())[case]
     cfg = M.ModelConfig(2, 4, 2, 8, 48, seed=0)
-    kv = KvPoolConfig(capacity_pages=120, page_bytes=64, chunk_pages=16, policy=KvPolicy.OFFLOAD)
-    rep = run_token_sim(_workload(4, 16, 24, seed=9), cfg, SimConfig(k=3, alpha=0.0, sparsity=0.4, max_batch=4),
-                        kv, check_lossless=True)
-    assert rep.emitted_tokens == 4 * 24
+    kv = KvPoolConfig(capacity_pages=gold["capacity"], page_bytes=64, chunk_pages=16, policy=KvPolicy.OFFLOAD)
+    n = gold["n"]
+    rep = run_token_sim(_workload(n, gold["input_len"], gold["output_len"], seed=gold["seed"]), cfg,
+                        SimConfig(k=3, alpha=0.0, sparsity=0.4, max_batch=n), kv, check_lossless=True)
+    assert rep.emitted_tokens == n * gold["output_len"]
+    assert {str(r): t for r, t in rep.outputs.items()} == gold["outputs"]
     assert max(r.offloaded_pages for r in rep.iterations) > 0
-    # the host tier is physical: K/V rows really left HBM and came back (outputs above are
-    # checked lossless against the autoregressive oracle)
     off, back = run_token_sim.last_transfer_bytes
     assert off > 0 and back > 0

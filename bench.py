@@ -276,19 +276,12 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         out["alpha"] = alpha_num / alpha_den if alpha_den else 0.0
 
         if with_roofline:
-            # roofline pass: CUDA events around every K1 / K2 launch, on the launching stream
+            # roofline pass: CUDA events recorded by the library's layer loop right around every
+            # K1 / K2 launch, on the launching stream (the launches run one after the other here;
+            # the timed region above overlaps them)
             ev = {"verify": [], "draft": []}
             bytes_acc = {"verify": 0.0, "draft": 0.0}
-
-            def timer(kind, begin):
-                e = torch.cuda.Event(enable_timing=True)
-                e.record(torch.cuda.current_stream())
-                if begin:
-                    ev[kind].append([e, None])
-                else:
-                    ev[kind][-1][1] = e
-
-            dec.attn_timer = timer
+            dec.attn_events = True
             # algorithmic bytes of each iteration's K1/K2 launches, from
             # the host-side batch plan right before the step
             mc = m.config
@@ -308,7 +301,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                 bytes_acc["verify"] += vb * L
                 bytes_acc["draft"] += db * L
                 one_iteration(dec)
+                for kind, pairs in dec.last_events.items():
+                    ev[kind].extend(pairs)
                 drain(dec)   # keep the host mirror exact for the next iteration's byte count
+            dec.attn_events = False
             torch.cuda.synchronize()
             for kind in ("verify", "draft"):
                 ms = [a.elapsed_time(b) for a, b in ev[kind] if b is not None]

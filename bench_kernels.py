@@ -6,9 +6,11 @@ GQA 4/8, d=128 (BASELINE.json configs[4]).
 
 One launch = one layer of a batch of requests.  Achieved GB/s = algorithmic
 bytes (K/V rows touched, q/o, lse, score accumulator writes)
-/ CUDA-event time, averaged over --iters launches after --warmup; the KV pool
-(> 126 MB L2 for every shape here) is rotated over 4 layers so consecutive
-launches do not hit in L2.  Prints one JSON line per shape.
+/ CUDA-event time, averaged over --iters launches after --warmup.  Before every
+timed launch a 256 MB buffer is written (L2 flush, 2x the 126 MB L2), which also
+keeps the GPU busy while the host enqueues the start event and the launch, so
+the event pair brackets the kernel alone (no host launch latency inside it).
+Prints one JSON line per shape.
 """
 
 from __future__ import annotations
@@ -73,6 +75,8 @@ def main():
         q = torch.randn(b * t, Hq, d, device=dev).to(torch.bfloat16)
         out = torch.empty_like(q)
 
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
         def timeit(fn):
             for _ in range(args.warmup):
                 fn(0)
@@ -80,6 +84,7 @@ def main():
             evs = []
             for i in range(args.iters):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                flush.zero_()   # L2 flush; the GPU is busy while the host enqueues e0 + launch
                 e0.record()
                 fn(i % args.layers)
                 e1.record()

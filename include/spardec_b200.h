@@ -218,16 +218,22 @@ typedef struct sd_attn_launch {
  * -> out-projection GEMM into the fp32 residual x -> rmsnorm -> MLP-in GEMM -> tanh ->
  * MLP-out GEMM into x.  GEMMs are cuBLAS (bf16 in, fp32 accumulate).  Buffers:
  * x fp32 [rows][h] (in/out); hn bf16 [rows][h]; qkv bf16 [rows][(q_heads+2kv_heads)d];
- * q, ctx bf16 [rows][q_heads][d]; hm bf16 [rows][2h]. */
-/* Workspace sd_forward_layers needs: the attention launches' (sd_attention_workspace_bytes,
- * max over the launches) plus a RoPE cos/sin table of `rows` rows kept at its end. */
-int64_t sd_forward_workspace_bytes(int32_t rows, int32_t head_dim, int64_t attention_bytes);
+ * q, ctx bf16 [rows][q_heads][d]; hm bf16 [rows][2h].
+ * Two launches (verify, draft) run concurrently per layer: the verify launch on a
+ * high-priority stream, the draft launch on a low-priority one (forked from / joined
+ * into `stream`), unless flags bit 0 is set or attn_events is given.
+ * attn_events (nullable): cudaEvent_t pairs [layers][num_launches][2] recorded around
+ * each attention launch (launches then run one after another). */
 int sd_forward_layers(const sd_layer_weights* weights, int32_t layers, float* x, void* hn, void* qkv, void* q,
                       void* ctx, void* hm, int32_t rows, int32_t hidden, int32_t q_heads,
                       const int32_t* row_table, const int32_t* row_pos, const sd_paged_kv* kv,
                       const sd_attn_launch* launches, int32_t num_launches, const int32_t* planted,
                       int32_t num_planted, float planted_bonus, float scale, float eps, void* workspace,
-                      int64_t workspace_bytes, void* stream);
+                      int64_t workspace_bytes, void* const* attn_events, int32_t flags, void* stream);
+
+/* Workspace sd_forward_layers needs: the attention launches' (sd_attention_workspace_bytes,
+ * max over the launches) plus a RoPE cos/sin table of `rows` rows kept at its end. */
+int64_t sd_forward_workspace_bytes(int32_t rows, int32_t head_dim, int64_t attention_bytes);
 
 #ifdef __cplusplus
 }

@@ -73,7 +73,7 @@ SIGNATURES = {
     "sd_forward_layers": (ctypes.c_int, [ctypes.POINTER(LayerWeights), _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                                          _i32, _i32, _i32, _c_p, _c_p, ctypes.POINTER(PagedKvDesc),
                                          ctypes.POINTER(AttnLaunchDesc), _i32, _c_p, _i32, ctypes.c_float,
-                                         ctypes.c_float, ctypes.c_float, _c_p, _i64, _c_p]),
+                                         ctypes.c_float, ctypes.c_float, _c_p, _i64, _c_p, _i32, _c_p]),
 }
 
 _LIB = None

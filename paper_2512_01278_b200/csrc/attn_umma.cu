@@ -87,6 +87,17 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
   const int TR = min(nt, TMAX);
   const int nfill = 3 * nt - TR;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cta_lin = blockIdx.y * gridDim.x + blockIdx.x;
+#define HTRACE(k, val)                                                                                  \
+  do {                                                                                                  \
+    if (p.trace && cta_lin < kTraceCtas) p.trace[cta_lin * kTraceSlots + (k)] = (val);                  \
+  } while (0)
+  if (tid == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    HTRACE(0, gtime());
+    HTRACE(9, (uint64_t)smid | ((uint64_t)nt << 32));
+  }
 
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -148,6 +159,7 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tptr;
+  if (tid == 0) HTRACE(1, gtime());
 
   const int64_t row_stride = (int64_t)p.kv.kv_heads * D;
   const __nv_bfloat16* Kg = static_cast<const __nv_bfloat16*>(p.kv.k) + (int64_t)p.layer * p.kv.layer_stride + h0 * D;
@@ -175,6 +187,7 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
       }
       cp_async_mbar_arrive(full + s);
     }
+    if (lane == 0) HTRACE(7, gtime());
     return;
   }
 
@@ -294,6 +307,10 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
     }
     lse[g] = m[g] + log2f(l[g]);
   }
+  if (tid == 0) {
+    HTRACE(2, gtime());
+    HTRACE(3, gtime());
+  }
 
   const bool scores = p.acc != nullptr && it.acc_row >= 0;
   for (int i2 = 0; i2 < nt; ++i2) {
@@ -338,9 +355,11 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
   }
 
   float o[NR];
+  if (tid == 0) HTRACE(4, gtime());
   if (nt > 0) {
     mbar_wait(obar, 0);
     tc_fence_after();
+    if (tid == 0) HTRACE(5, gtime());
     tmem_ld_row<NR>(tl + OCOL, o);
   } else {
 #pragma unroll
@@ -355,6 +374,8 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
 #pragma unroll
     for (int g = 0; g < G; ++g) p.lse_out[(int64_t)it.q_row0 * p.q_heads + (h0 + hh) * G + g] = lse[g] * LN2;
   }
+  if (tid == 0) HTRACE(6, gtime());
+#undef HTRACE
 }
 
 template <int G, int HPC, int NSLOT, int TCOLS>
@@ -370,6 +391,7 @@ int launch_hp(const Params& prm, int num_items, int kv_heads, int ct, cudaStream
   static int configured = 0;
   if (smem > configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // as K2: no reconfig
     configured = smem;
   }
   kern<<<dim3(kv_heads / HPC, num_items), NT, smem, stream>>>(prm);
@@ -556,6 +578,11 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
   prm.q_heads = q_heads;
   prm.scale_log2 = scale * LOG2E;
   const int G = q_heads / kvp->kv_heads;
+  static const int trace = env_int("SD_ATTN_TRACE", 0);
+  if (trace) {
+    if (g_trace_buf == nullptr) cudaMalloc(&g_trace_buf, sizeof(uint64_t) * kTraceCtas * kTraceSlots);
+    prm.trace = g_trace_buf;
+  }
   static const int hp_env = env_int("SD_UMMA_HP", 1);
   if (hp_env && max_nq == 1 && kvp->dtype == SD_DTYPE_BF16 && kvp->head_dim == D && (G == 4 || G == 8) &&
       kvp->kv_heads % 4 == 0) {
@@ -581,11 +608,6 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
   if (!umma_plan(kvp, num_items, max_keys, max_nq, q_heads, dense, &pl)) return 0;
   prm.chunk = pl.chunk;
   prm.dense = dense;
-  static const int trace = env_int("SD_ATTN_TRACE", 0);
-  if (trace) {
-    if (g_trace_buf == nullptr) cudaMalloc(&g_trace_buf, sizeof(uint64_t) * kTraceCtas * kTraceSlots);
-    prm.trace = g_trace_buf;
-  }
   *handled = true;
   return G == 4 ? launch_verify_g4(prm, pl.NR, pl.C, num_items, kvp->kv_heads, stream)
                 : launch_verify_g8(prm, pl.NR, pl.C, num_items, kvp->kv_heads, stream);

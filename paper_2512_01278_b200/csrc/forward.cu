@@ -46,8 +46,14 @@ __global__ void tanh_bf16_kernel(__nv_bfloat16* x, int64_t n) {
     for (int64_t j = i; j < n; ++j) x[j] = __float2bfloat16_rn(tanhf(__bfloat162float(x[j])));
 }
 
+// one handle (+ workspace) per (thread, device): a handle and its workspace are bound to the
+// device current at creation
 static cublasHandle_t handle_for_thread() {
-  static thread_local cublasHandle_t h = nullptr;
+  constexpr int kMaxDev = 16;
+  static thread_local cublasHandle_t hs[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  cublasHandle_t& h = hs[dev];
   if (h == nullptr) {
     if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
     cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);
@@ -77,7 +83,48 @@ static int gemm(cublasHandle_t hd, int R, int N, int K, const void* A, const voi
   return 0;
 }
 
+// Side streams for the attention launches of one layer: the verify launch (K2) on a
+// high-priority stream, the draft launch (K1) on a low-priority one, both forked from and
+// joined back into the caller's stream, so the block scheduler hands free CTA slots to K2
+// first and K1's CTAs fill K2's tail waves (one per (thread, device)).
+struct AttnStreams {
+  cudaStream_t hi = nullptr, lo = nullptr;
+  cudaEvent_t fork = nullptr, join_hi = nullptr, join_lo = nullptr;
+};
+
+static AttnStreams* attn_streams() {
+  constexpr int kMaxDev = 16;
+  static thread_local AttnStreams st[kMaxDev];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  AttnStreams& a = st[dev];
+  if (a.hi == nullptr) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (cudaStreamCreateWithPriority(&a.hi, cudaStreamNonBlocking, greatest) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&a.lo, cudaStreamNonBlocking, least) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a.join_hi, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a.join_lo, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      a = AttnStreams{};
+      return nullptr;
+    }
+  }
+  return &a;
+}
+
 }  // namespace sd
+
+namespace {
+int attn_launch(const sd_attn_launch& a, const void* q, void* ctx, const sd_paged_kv* kv, int l,
+                const int32_t* planted, int32_t num_planted, float planted_bonus, int32_t q_heads, float scale,
+                void* workspace, int64_t workspace_bytes, cudaStream_t s) {
+  return sd_attention(q, ctx, nullptr, kv, l, a.items, a.num_items, a.max_keys, a.max_nq, a.crit, a.acc,
+                      a.acc_row_stride, a.acc_shift, planted, num_planted, planted_bonus, q_heads, scale, workspace,
+                      workspace_bytes, 0, s);
+}
+}  // namespace
 
 extern "C" int64_t sd_forward_workspace_bytes(int32_t rows, int32_t head_dim, int64_t attention_bytes) {
   return ((attention_bytes + 255) / 256) * 256 + sd::rope_table_bytes(rows, head_dim);
@@ -88,7 +135,7 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
                                  const int32_t* row_table, const int32_t* row_pos, const sd_paged_kv* kv,
                                  const sd_attn_launch* launches, int32_t num_launches, const int32_t* planted,
                                  int32_t num_planted, float planted_bonus, float scale, float eps, void* workspace,
-                                 int64_t workspace_bytes, void* stream) {
+                                 int64_t workspace_bytes, void* const* attn_events, int32_t flags, void* stream) {
   SD_REQUIRE(w != nullptr && x != nullptr && kv != nullptr, "sd_forward_layers: null pointer");
   SD_REQUIRE(kv->dtype == SD_DTYPE_BF16, "sd_forward_layers: bf16 pools only (fp32 parity mode runs in torch)");
   SD_REQUIRE(rows > 0 && layers > 0 && num_launches >= 0, "sd_forward_layers: bad sizes");
@@ -110,6 +157,11 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
     table = reinterpret_cast<float2*>(static_cast<char*>(workspace) + workspace_bytes);
     sd::rope_table(row_pos, rows, kv->head_dim, table, s);
   }
+  // two attention launches (verify + draft) overlap on priority streams unless timed per
+  // launch (attn_events) or disabled (flags bit 0)
+  sd::AttnStreams* as = nullptr;
+  const bool overlap = num_launches == 2 && attn_events == nullptr && !(flags & 1) &&
+                       launches[0].num_items > 0 && launches[1].num_items > 0 && (as = sd::attn_streams()) != nullptr;
   int rc;
   for (int l = 0; l < layers; ++l) {
     if ((rc = sd_rmsnorm_cast(x, rows, hidden, eps, hn, SD_DTYPE_BF16, stream)) != 0) return rc;
@@ -118,13 +170,32 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
       sd::rope_kv_write_table(qkv, qkv_w, rows, row_table, row_pos, kv, l, q_heads, table, q, s);
     else if ((rc = sd_rope_kv_write(qkv, qkv_w, rows, row_table, row_pos, kv, l, q_heads, q, stream)) != 0)
       return rc;
-    for (int i = 0; i < num_launches; ++i) {
-      const sd_attn_launch& a = launches[i];
-      if (a.num_items == 0) continue;
-      if ((rc = sd_attention(q, ctx, nullptr, kv, l, a.items, a.num_items, a.max_keys, a.max_nq, a.crit, a.acc,
-                             a.acc_row_stride, a.acc_shift, planted, num_planted, planted_bonus, q_heads, scale,
-                             workspace, workspace_bytes, 0, stream)) != 0)
+    if (overlap) {
+      // K2 (launch 0) high priority, K1 (launch 1) low priority, concurrently
+      cudaEventRecord(as->fork, s);
+      cudaStreamWaitEvent(as->hi, as->fork, 0);
+      cudaStreamWaitEvent(as->lo, as->fork, 0);
+      if ((rc = attn_launch(launches[0], q, ctx, kv, l, planted, num_planted, planted_bonus, q_heads, scale,
+                            workspace, workspace_bytes, as->hi)) != 0)
         return rc;
+      if ((rc = attn_launch(launches[1], q, ctx, kv, l, planted, num_planted, planted_bonus, q_heads, scale,
+                            workspace, workspace_bytes, as->lo)) != 0)
+        return rc;
+      cudaEventRecord(as->join_hi, as->hi);
+      cudaEventRecord(as->join_lo, as->lo);
+      cudaStreamWaitEvent(s, as->join_hi, 0);
+      cudaStreamWaitEvent(s, as->join_lo, 0);
+    } else {
+      for (int i = 0; i < num_launches; ++i) {
+        const sd_attn_launch& a = launches[i];
+        if (a.num_items == 0) continue;
+        cudaEvent_t* ev = attn_events ? (cudaEvent_t*)(attn_events + 2 * ((int64_t)l * num_launches + i)) : nullptr;
+        if (ev && ev[0]) cudaEventRecord(ev[0], s);
+        if ((rc = attn_launch(a, q, ctx, kv, l, planted, num_planted, planted_bonus, q_heads, scale, workspace,
+                              workspace_bytes, s)) != 0)
+          return rc;
+        if (ev && ev[1]) cudaEventRecord(ev[1], s);
+      }
     }
     if ((rc = sd::gemm(hd, rows, hidden, hidden, ctx, w[l].wo, x, true, 1.f)) != 0) return rc;
     if ((rc = sd_rmsnorm_cast(x, rows, hidden, eps, hn, SD_DTYPE_BF16, stream)) != 0) return rc;

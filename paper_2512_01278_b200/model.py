@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes
 
 import math
+import os
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -226,7 +227,8 @@ class AttnLaunch:
     acc: torch.Tensor | None = None  # int64 fixed-point score accumulators (unit 2^-acc_shift)
     acc_row_stride: int = 0
     acc_shift: int = 0
-    timer: object | None = None   # optional callable(start: bool) for per-launch timing
+    timer: object | None = None   # optional callable(start: bool) for per-launch timing (torch loop)
+    events: list | None = None    # optional [(start, end) torch.cuda.Event] per layer (native loop)
 
 
 # Overlapping the verify and draft launches of a layer on two streams was measured SLOWER
@@ -265,6 +267,8 @@ def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_t
     if (NATIVE_FORWARD and dt == torch.bfloat16 and lse_out is None and not force_generic and q_trace is None
             and all(ln.timer is None for ln in launches)):
         return _forward_native(model, pool, tokens, row_table, row_pos, launches, x)
+    if any(ln.events is not None for ln in launches):
+        raise ContractError("per-launch events are recorded by the native (bf16) layer loop only")
     hn = torch.empty(R, c.hidden_dim, dtype=dt, device=model.device)
     q_buf = torch.empty(R, Hq, d, dtype=dt, device=model.device)
     ctx = torch.empty(R, Hq, d, dtype=dt, device=model.device)
@@ -313,6 +317,9 @@ def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_t
 
 
 NATIVE_FORWARD = True  # bf16: the layer loop runs in the library (sd_forward_layers), one host call
+# verify (K2) and draft (K1) launches of a layer concurrently on priority streams: measured
+# 2823 vs 2858 tok/s serial (configs[1]), so off unless SD_ATTN_OVERLAP=1
+OVERLAP_ATTENTION = os.environ.get("SD_ATTN_OVERLAP", "0") == "1"
 # query rows (tokens x GQA group) per attention work item for multi-token windows (prefill,
 # forward_full): <= 48 keeps the tcgen05 verify kernel at two CTAs per SM
 ITEM_ROWS = 48
@@ -358,11 +365,23 @@ def _forward_native(model: ToyModel, pool: PagedKvPool, tokens, row_table, row_p
     ctx = torch.empty(R, Hq, d, dtype=dt, device=dev)
     hm = torch.empty(R, 2 * h, dtype=dt, device=dev)
     n_planted = 0 if model.planted_dev is None else model.planted_dev.numel()
+    ev_arr = None
+    if any(ln.events is not None for ln in launches):
+        # cudaEvent_t pairs [layer][launch][2] recorded around each attention launch
+        ev_arr = (ctypes.c_void_p * (2 * c.num_layers * len(launches)))()
+        for i, ln in enumerate(launches):
+            if ln.events is None:
+                continue
+            for l, (e0, e1) in enumerate(ln.events):
+                ev_arr[2 * (l * len(launches) + i)] = e0.cuda_event
+                ev_arr[2 * (l * len(launches) + i) + 1] = e1.cuda_event
+    flags = 0 if OVERLAP_ATTENTION else 1
     N.check(lib.sd_forward_layers(wts, c.num_layers, x.data_ptr(), hn.data_ptr(), qkv.data_ptr(), q.data_ptr(),
                                   ctx.data_ptr(), hm.data_ptr(), R, h, Hq, row_table.data_ptr(), row_pos.data_ptr(),
                                   ctypes.byref(desc), descs, len(launches), N.ptr(model.planted_dev), n_planted,
                                   model.planted_bonus, 1.0 / math.sqrt(d), RMS_EPS, N.ptr(ws),
-                                  0 if ws is None else ws.numel(), N.stream_handle()), "sd_forward_layers")
+                                  0 if ws is None else ws.numel(), ev_arr, flags, N.stream_handle()),
+            "sd_forward_layers")
     return x
 
 

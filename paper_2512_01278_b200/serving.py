@@ -149,7 +149,11 @@ class BatchedDecoder:
         self._host_kv: dict = {}     # request -> {position: (K rows, V rows)} pinned host copies
         self.offloaded_bytes = 0
         self.reloaded_bytes = 0
-        self.attn_timer = None       # optional callable(kind, start) for per-launch timing
+        self.attn_timer = None       # optional callable(kind, start) for per-launch timing (torch loop)
+        self.attn_events = False     # record (start, end) events around every K1 / K2 launch
+        self.keep_logits = False     # keep the last step's logits (diagnostics)
+        self.last_logits = None
+        self.last_events: dict = {}  # kind -> [(start, end)] per layer of the last submitted step
         self.host_times: list = []   # per step: (host enqueue s, enqueue + device drain s)
         self.last_rows = 0
 
@@ -452,16 +456,33 @@ class BatchedDecoder:
                        self.drafted_dev, self.crit_len_dev, self._tok_buf, self._rt_buf, self._rp_buf,
                        self._v_items, self._d_items, self.acc, self.acc.stride(0))
         launches = []
+        self.last_events = {}
+
+        def events(kind):
+            if not self.attn_events:
+                return None
+            evs = []
+            for _ in range(c.num_layers):
+                pair = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for e in pair:
+                    e.record()  # materialise the CUDA event; re-recorded around the launch
+                evs.append(pair)
+            self.last_events[kind] = evs
+            return evs
+
         if verifs:
             launches.append(AttnLaunch(self._v_items, len(verifs), v_max_keys, v_max_nq, acc=self.acc,
                                        acc_row_stride=self.acc_w, acc_shift=self.verify_shift,
-                                       timer=self._timer("verify")))
-        if drafts:  # after the verify launch: it runs on the side stream (model.forward_rows)
+                                       timer=self._timer("verify"), events=events("verify")))
+        if drafts:  # launch 1: overlaps the verify launch on a low-priority stream
             launches.append(AttnLaunch(self._d_items, len(drafts), d_max_keys, 1, crit=self.crit,
-                                       timer=self._timer("draft")))
+                                       timer=self._timer("draft"), events=events("draft")))
         x = forward_rows(self.model, self.pool, self._tok_buf[:R], self._rt_buf[:R], self._rp_buf[:R], launches)
         targets = self._targets[:R]
-        K.argmax_rows(lm_head(self.model, x).contiguous(), targets)
+        logits = lm_head(self.model, x).contiguous()
+        K.argmax_rows(logits, targets)
+        if self.keep_logits:   # diagnostics (tools/alpha_margin.py): rows in plan order
+            self.last_logits = logits
         sel_rows, sel_kv, sel_slot = self._sel[0], self._sel[1], self._sel[2]
         K.step_commit(plan_dev, n_members, self.k, targets, self.n_kv_dev, self.last_tok_dev, self.drafted_dev,
                       sel_rows, sel_kv, sel_slot, self._res_dev)

@@ -1,4 +1,8 @@
 #!/bin/bash
+# compute-sanitizer on a tiny K2 (2-CTA cluster) + K1 launch (tools/race_small.py)
 mkdir -p gpurun_out
 CS=/usr/local/cuda/bin/compute-sanitizer
-timeout 2400 $CS --tool racecheck --racecheck-report analysis --target-processes all python -m pytest tests/test_kernels_gpu.py -q -x -k "(test_verify_attention_matches_oracle and False-128) or test_batched_items_mixed_lengths_bf16" > gpurun_out/san_racecheck.log 2>&1; echo "rc=$?" >> gpurun_out/san_racecheck.log
+for tool in racecheck synccheck memcheck; do
+  SD_ATTN_C=2 timeout 1200 $CS --tool $tool --target-processes all python tools/race_small.py \
+    > gpurun_out/san_$tool.log 2>&1; echo "rc=$?" >> gpurun_out/san_$tool.log
+done

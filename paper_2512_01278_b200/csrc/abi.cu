@@ -22,7 +22,7 @@ bool umma_supported(const sd_paged_kv* kvp, int max_nq, int q_heads);
 int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer, const int32_t* items,
                      int num_items, int max_keys, int max_nq, const int32_t* crit, unsigned long long* acc,
                      int64_t acc_stride, int acc_shift, const int32_t* planted, int n_planted, float bonus,
-                     int q_heads, float scale, cudaStream_t stream, bool* handled);
+                     int q_heads, float scale, void* ws, int64_t ws_bytes, cudaStream_t stream, bool* handled);
 
 }  // namespace sd
 
@@ -66,7 +66,7 @@ extern "C" int sd_attention(const void* q, void* out, float* lse, const sd_paged
     bool handled = false;
     const int rc = sd::launch_attn_umma(q, out, lse, kv, layer, items, num_items, max_keys, max_nq, crit, a,
                                         acc_row_stride, acc_shift, planted, num_planted, planted_bonus, q_heads,
-                                        scale, s, &handled);
+                                        scale, workspace, workspace_bytes, s, &handled);
     if (handled || rc != 0) return rc;
   }
   return sd::launch_attn_generic(q, out, lse, kv, layer, items, num_items, max_keys, max_nq, crit, a,

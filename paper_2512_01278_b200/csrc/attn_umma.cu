@@ -404,39 +404,6 @@ int launch_hp(const Params& prm, int num_items, int kv_heads, int ct, cudaStream
   return 0;
 }
 
-template <int G, int NR, int NSLOT, int TCOLS>
-int launch_one(const Params& prm, int C, int num_items, int kv_heads, cudaStream_t stream) {
-  constexpr int TMAX = (TCOLS - NR) / NR;
-  auto kern = attn_umma_kernel<G, NR, NSLOT, TCOLS>;
-  const int smem = make_layout(NR, NSLOT, TMAX, prm.chunk / TK, prm.dense).total;
-  static int configured = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // two CTAs per SM
-    configured = smem;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(C, kv_heads, num_items);
-  cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm);
-  count_launch();
-  if (e != cudaSuccess) {
-    set_error(std::string("sd_attention (umma) launch: ") + cudaGetErrorString(e));
-    return (int)e;
-  }
-  return 0;
-}
-
 static uint64_t* g_trace_buf = nullptr;  // SD_ATTN_TRACE=1: per-CTA phase timestamps
 
 static int env_int(const char* name, int dflt) {
@@ -558,7 +525,7 @@ bool umma_supported(const sd_paged_kv* kvp, int max_nq, int q_heads) {
 int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kvp, int layer, const int32_t* items,
                      int num_items, int max_keys, int max_nq, const int32_t* crit, unsigned long long* acc,
                      int64_t acc_stride, int acc_shift, const int32_t* planted, int n_planted, float bonus,
-                     int q_heads, float scale, cudaStream_t stream, bool* handled) {
+                     int q_heads, float scale, void* ws, int64_t ws_bytes, cudaStream_t stream, bool* handled) {
   using namespace umma_attn;
   *handled = false;
   Params prm{};
@@ -603,8 +570,8 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
                    : launch_hp<8, 4, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
     }
   }
-  UmmaPlan pl;
   const int dense = (crit == nullptr && kvp->page_shift >= 4) ? 1 : 0;
+  UmmaPlan pl;
   if (!umma_plan(kvp, num_items, max_keys, max_nq, q_heads, dense, &pl)) return 0;
   prm.chunk = pl.chunk;
   prm.dense = dense;

@@ -654,6 +654,7 @@ constexpr int kMaxNR = 80;
 int launch_verify_g4(const Params& prm, int NR, int C, int num_items, int kv_heads, cudaStream_t stream);
 int launch_verify_g8(const Params& prm, int NR, int C, int num_items, int kv_heads, cudaStream_t stream);
 int verify_slots_g4(int NR, int C, int smem);
+
 int verify_slots_g8(int NR, int C, int smem);
 
 }  // namespace umma_attn

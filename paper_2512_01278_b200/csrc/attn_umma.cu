@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <tuple>
 
+#include <cuda.h>
+
 namespace sd {
 namespace umma_attn {
 
@@ -379,7 +381,7 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
 }
 
 template <int G, int HPC, int NSLOT, int TCOLS>
-__global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_hp_kernel(const Params p) {
+__global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_hp_kernel(const __grid_constant__ Params p) {
   draft_body<G, HPC, NSLOT, TCOLS>(p, blockIdx.x, blockIdx.y);
 }
 
@@ -453,6 +455,46 @@ static bool plan_umma(int max_keys, int num_items, int kv_heads, int S, int cap,
   if (best == 0) return false;
   *C_out = best;
   *chunk_out = ((tiles + best - 1) / best) * TK;
+  return true;
+}
+
+// TMA descriptors of one layer's K or V pool: [slots][kv heads][128] bf16, 16 x 1 x 64 boxes,
+// SWIZZLE_128B (the UMMA K-major tile layout); cached per (base, slots, heads)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static bool pool_map(CUtensorMap* out, const void* base, int64_t slots, int kv_heads) {
+  static std::mutex mu;
+  static EncodeTiledFn encode = nullptr;
+  static std::map<std::tuple<uintptr_t, int64_t, int>, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(base), slots, kv_heads);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  if (encode == nullptr) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || fn == nullptr) {
+      cudaGetLastError();
+      return false;
+    }
+    encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)umma_attn::D, (cuuint64_t)kv_heads, (cuuint64_t)slots};
+  const cuuint64_t strides[2] = {(cuuint64_t)umma_attn::D * 2, (cuuint64_t)kv_heads * umma_attn::D * 2};
+  const cuuint32_t box[3] = {64, 1, 16};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap m;
+  if (encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (cache.size() > 4096) cache.clear();
+  cache[key] = m;
+  *out = m;
   return true;
 }
 
@@ -571,6 +613,12 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
     }
   }
   const int dense = (crit == nullptr && kvp->page_shift >= 4) ? 1 : 0;
+  static const int tma_env = env_int("SD_K2_TMA", 1);
+  if (dense && tma_env) {  // dense K2 chunks stream through TMA boxes (one descriptor per pool and layer)
+    const int64_t loff = (int64_t)layer * kvp->layer_stride * 2;  // bytes (bf16)
+    prm.tma = pool_map(&prm.tmk, static_cast<const char*>(kvp->k) + loff, kvp->num_slots, kvp->kv_heads) &&
+              pool_map(&prm.tmv, static_cast<const char*>(kvp->v) + loff, kvp->num_slots, kvp->kv_heads);
+  }
   UmmaPlan pl;
   if (!umma_plan(kvp, num_items, max_keys, max_nq, q_heads, dense, &pl)) return 0;
   prm.chunk = pl.chunk;

@@ -163,7 +163,7 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
   // ---- setup ----
   if (warp == WMMA) tmem_alloc(tptr, TCOLS);
   if (tid == 0) {
-    for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, 32), mbar_init(empty + i, 1);
+    for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, 1), mbar_init(empty + i, 1);
     for (int i = 0; i < S; ++i) mbar_init(sfull + i, 1), mbar_init(sfree + i, NSW);
     mbar_init(pready + 0, NSW), mbar_init(pready + 1, NSW);
     mbar_init(pfree + 0, 1), mbar_init(pfree + 1, 1);
@@ -241,24 +241,46 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
     const int sub = lane >> 4, c = lane & 15;   // 2 key rows x 16 chunks per instruction
     const uint32_t ring_u = smem_u32(ring);
     const int nfill = sc.nfill();
+    // dense chunks starting on a 16-key boundary: TMA boxes of 16 keys (lanes 0-7 issue the two
+    // 64-element halves of one box each); otherwise 16-byte cp.async of every row
+    const bool use_tma = p.tma && p.dense && ((it.dense_lo + kb) & 15) == 0;
     for (int f = 0; f < nfill; ++f) {
       const int s = f % NSLOT;
       int t;
       bool isv;
       sc.fill(f, t, isv);
-      const __nv_bfloat16* base = (isv ? Vg : Kg) + c * 8;
-      int sl[4];  // physical slots of keys lane + 32m, broadcast by shuffles below
+      const uint32_t tile_u = ring_u + s * TILE_BYTES;
+      if (use_tma) {
+        int slot0 = 0;
+        if (lane < TK / 16) {
+          const int pos = it.dense_lo + min(kb + t * TK + lane * 16, ke - 1);
+          slot0 = ((spage[(pos >> pshift) - dpage0] << pshift) | (pos & pmask)) & ~15;
+        }
+        if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
+        if (lane < TK / 16) {
+          const CUtensorMap* map = isv ? &p.tmv : &p.tmk;
+          tma_box(tile_u + lane * 2048, map, 0, h, slot0, full + s, pol);
+          tma_box(tile_u + TK * 128 + lane * 2048, map, 64, h, slot0, full + s, pol);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_tx(full + s, TILE_BYTES);
+      } else {
+        const __nv_bfloat16* base = (isv ? Vg : Kg) + c * 8;
+        int sl[4];  // physical slots of keys lane + 32m, broadcast by shuffles below
 #pragma unroll
-      for (int m = 0; m < 4; ++m) sl[m] = slot_of(t * TK + m * 32 + lane);
-      if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
-      const uint32_t dst0 = ring_u + s * TILE_BYTES + (c >> 3) * (TK * 128);
+        for (int m = 0; m < 4; ++m) sl[m] = slot_of(t * TK + m * 32 + lane);
+        if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
+        const uint32_t dst0 = tile_u + (c >> 3) * (TK * 128);
 #pragma unroll
-      for (int kk = 0; kk < TK / 2; ++kk) {
-        const int i = 2 * kk + sub;  // key row within the tile
-        const int slot = __shfl_sync(0xffffffffu, sl[kk >> 4], i & 31);
-        cp_async16(dst0 + i * 128 + (((c & 7) ^ (i & 7)) << 4), base + (int64_t)slot * row_stride, pol);
+        for (int kk = 0; kk < TK / 2; ++kk) {
+          const int i = 2 * kk + sub;  // key row within the tile
+          const int slot = __shfl_sync(0xffffffffu, sl[kk >> 4], i & 31);
+          cp_async16(dst0 + i * 128 + (((c & 7) ^ (i & 7)) << 4), base + (int64_t)slot * row_stride, pol);
+        }
+        cp_async_mbar_arrive_inc(full + s);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(full + s);
       }
-      cp_async_mbar_arrive(full + s);
       if (f == nt - 1) {
         if (lane == 0) TRACE(11, gtime());
         if (C > 1) {
@@ -577,7 +599,7 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
 }
 
 template <int G, int NR, int NSLOT, int TCOLS>
-__global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(const Params p) {
+__global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(const __grid_constant__ Params p) {
   verify_body<G, NR, NSLOT, TCOLS>(p, blockIdx.y, blockIdx.z);
 }
 

@@ -2,6 +2,7 @@
 // mbarriers, cp.async, TMEM, UMMA descriptors, launch parameters and the smem layout.
 #pragma once
 #include <cooperative_groups.h>
+#include <cuda.h>
 
 #include "common.cuh"
 
@@ -40,6 +41,22 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64
 }
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// the barrier tracks this thread's prior cp.async copies (pending count +1, then the async arrival)
+__device__ __forceinline__ void cp_async_mbar_arrive_inc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// TMA: one 16-key x 64-element box of a K or V page into the SWIZZLE_128B tile layout
+__device__ __forceinline__ void tma_box(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                        uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
@@ -143,6 +160,9 @@ __device__ __forceinline__ uint64_t gtime() {
 }
 
 struct Params {
+  CUtensorMap tmk;  // dense items: the layer's K / V pool as [slots][kv heads][128] bf16,
+  CUtensorMap tmv;  // 16-slot x 1-head x 64-element boxes, SWIZZLE_128B (valid when tma)
+  int tma;
   uint64_t* trace;  // diagnostics: [kTraceCtas][kTraceSlots] per-CTA phase timestamps, or null
   const __nv_bfloat16* q;
   __nv_bfloat16* out;
@@ -161,6 +181,7 @@ struct Params {
   float scale_log2;
   int chunk;  // keys per CTA, multiple of TK
   int dense;  // 1: items have no critical list and pages >= 16 tokens (page ids staged, not slots)
+  int dbg;    // diagnostics (SD_ATTN_DBG): timing experiments only
 };
 
 // (m, l) softmax-statistics merge

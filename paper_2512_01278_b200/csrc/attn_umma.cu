@@ -72,6 +72,11 @@ __host__ __device__ inline Layout make_hp_layout(int NR, int NSLOT, int TMAX, in
   return L;
 }
 
+// head-packed kernel warp layout: softmax warps 0-3, HP_NPROD producer warps, the MMA warp
+constexpr int HP_NPROD = 4;
+constexpr int HP_WPROD = NSW, HP_WMMA = NSW + HP_NPROD;
+constexpr int HP_NT = (NSW + HP_NPROD + 1) * 32;
+
 template <int G, int HPC, int NSLOT, int TCOLS>
 __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, const int item_idx) {
   constexpr int NQ = HPC * G;                       // q heads of the CTA
@@ -118,9 +123,9 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
   uint64_t* obar = pfree + 2;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L.tptr);
 
-  if (warp == WMMA) tmem_alloc(tptr, TCOLS);
+  if (warp == HP_WMMA) tmem_alloc(tptr, TCOLS);
   if (tid == 0) {
-    for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, 32), mbar_init(empty + i, 1);
+    for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, 32 * HP_NPROD), mbar_init(empty + i, 1);
     for (int i = 0; i < TMAX; ++i) mbar_init(sfull + i, 1), mbar_init(sfree + i, NSW);
     mbar_init(pready + 0, NSW), mbar_init(pready + 1, NSW);
     mbar_init(pfree + 0, 1), mbar_init(pfree + 1, 1);
@@ -131,15 +136,15 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
     const int nkeys = nt * KPT;
     const int32_t* trow = p.kv.table + (int64_t)it.table_row * p.kv.table_stride;
     const int pmask = (1 << p.kv.page_shift) - 1;
-    for (int j0 = 0; j0 < nkeys; j0 += 8 * NT) {
+    for (int j0 = 0; j0 < nkeys; j0 += 8 * HP_NT) {
       int pos[8], pg[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) pos[k] = it.key_pos(p.crit, min(j0 + k * NT + tid, nk - 1));
+      for (int k = 0; k < 8; ++k) pos[k] = it.key_pos(p.crit, min(j0 + k * HP_NT + tid, nk - 1));
 #pragma unroll
       for (int k = 0; k < 8; ++k) pg[k] = __ldg(trow + (pos[k] >> p.kv.page_shift));
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const int j = j0 + k * NT + tid;
+        const int j = j0 + k * HP_NT + tid;
         if (j < nkeys) {
           spos[j] = j < nk ? pos[k] : -1;
           sslot[j] = (pg[k] << p.kv.page_shift) | (pos[k] & pmask);
@@ -148,14 +153,14 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
     }
   }
   // Q: the CTA's NQ q heads are contiguous in the row (heads h0.. x group)
-  for (int i = tid; i < NR * 16; i += NT) {
+  for (int i = tid; i < NR * 16; i += HP_NT) {
     const int r = i >> 4, c = i & 15;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (r < NQ) v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)it.q_row0 * p.q_heads + h0 * G + r) * D + c * 8);
     *reinterpret_cast<uint4*>(qs + (c >> 3) * (NR * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
   }
   // P^T buffers: off-diagonal blocks stay zero for the whole launch
-  for (int i = tid; i < 2 * NR * TK * 2 / 16; i += NT) reinterpret_cast<uint4*>(pbuf)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < 2 * NR * TK * 2 / 16; i += HP_NT) reinterpret_cast<uint4*>(pbuf)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async();
   tc_fence_before();
   __syncthreads();
@@ -167,10 +172,13 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
   const __nv_bfloat16* Kg = static_cast<const __nv_bfloat16*>(p.kv.k) + (int64_t)p.layer * p.kv.layer_stride + h0 * D;
   const __nv_bfloat16* Vg = static_cast<const __nv_bfloat16*>(p.kv.v) + (int64_t)p.layer * p.kv.layer_stride + h0 * D;
 
-  if (warp == WPROD) {
+  if (warp >= HP_WPROD && warp < HP_WPROD + HP_NPROD) {
+    // producers: warp pw copies rows [pw * 128 / HP_NPROD, ...) of every 32 KB fill (one head's keys)
+    const int pw = warp - HP_WPROD;
     const uint64_t pol = policy_evict_first();
     const int sub = lane >> 4, c = lane & 15;
     const uint32_t ring_u = smem_u32(ring);
+    constexpr int KK = TK / 2 / HP_NPROD;  // row pairs per warp
     for (int f = 0; f < nfill; ++f) {
       const int s = f % NSLOT;
       int t;
@@ -181,7 +189,8 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
       if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
       const uint32_t dst0 = ring_u + s * TILE_BYTES + (c >> 3) * (TK * 128);
 #pragma unroll
-      for (int kk = 0; kk < TK / 2; ++kk) {
+      for (int k2 = 0; k2 < KK; ++k2) {
+        const int kk = pw * KK + k2;
         const int i = 2 * kk + sub;            // tile row = head-major (hh, key)
         const int hh = (2 * kk) / KPT;         // same for both rows of the instruction
         const int slot = __shfl_sync(0xffffffffu, sl, ((2 * kk) % KPT) + sub);
@@ -189,11 +198,11 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
       }
       cp_async_mbar_arrive(full + s);
     }
-    if (lane == 0) HTRACE(7, gtime());
+    if (pw == 0 && lane == 0) HTRACE(7, gtime());
     return;
   }
 
-  if (warp == WMMA) {
+  if (warp == HP_WMMA) {
     const uint32_t ring_u = smem_u32(ring), q_u = smem_u32(qs), p_u = smem_u32(pbuf);
     const uint32_t id_qk = idesc_bf16(NR, false, false);
     const uint32_t id_pv = idesc_bf16(NR, true, true);
@@ -381,7 +390,7 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
 }
 
 template <int G, int HPC, int NSLOT, int TCOLS>
-__global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_hp_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(HP_NT, TCOLS == 512 ? 1 : 2) attn_umma_hp_kernel(const __grid_constant__ Params p) {
   draft_body<G, HPC, NSLOT, TCOLS>(p, blockIdx.x, blockIdx.y);
 }
 
@@ -396,7 +405,7 @@ int launch_hp(const Params& prm, int num_items, int kv_heads, int ct, cudaStream
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // as K2: no reconfig
     configured = smem;
   }
-  kern<<<dim3(kv_heads / HPC, num_items), NT, smem, stream>>>(prm);
+  kern<<<dim3(kv_heads / HPC, num_items), HP_NT, smem, stream>>>(prm);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

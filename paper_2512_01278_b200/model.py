@@ -317,9 +317,11 @@ def forward_rows(model: ToyModel, pool: PagedKvPool, tokens: torch.Tensor, row_t
 
 
 NATIVE_FORWARD = True  # bf16: the layer loop runs in the library (sd_forward_layers), one host call
-# verify (K2) and draft (K1) launches of a layer concurrently on priority streams: measured
-# 2823 vs 2858 tok/s serial (configs[1]), so off unless SD_ATTN_OVERLAP=1
-OVERLAP_ATTENTION = os.environ.get("SD_ATTN_OVERLAP", "0") == "1"
+# verify (K2) and draft (K1) launches of a layer concurrently on priority streams (K1's CTAs
+# fill K2's tail waves): configs[1] 2970 vs 2907 tok/s serial with the TMA K2 producer and
+# the four-warp K1 producer (round 2; round 1's kernels measured 2823 vs 2858), so on unless
+# SD_ATTN_OVERLAP=0
+OVERLAP_ATTENTION = os.environ.get("SD_ATTN_OVERLAP", "1") == "1"
 # query rows (tokens x GQA group) per attention work item for multi-token windows (prefill,
 # forward_full): <= 48 keeps the tcgen05 verify kernel at two CTAs per SM
 ITEM_ROWS = 48

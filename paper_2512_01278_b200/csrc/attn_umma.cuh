@@ -160,10 +160,15 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
   float* rowlse = reinterpret_cast<float*>(smem + L.rowlse);
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L.tptr);
 
+  // dense chunks starting on a 16-key boundary stream through TMA boxes of 16 keys (producer
+  // lanes 0-7 issue the two 64-element halves of one box each); otherwise 16-byte cp.async
+  const bool use_tma = p.tma && p.dense && ((it.dense_lo + kb) & 15) == 0;
+
   // ---- setup ----
   if (warp == WMMA) tmem_alloc(tptr, TCOLS);
   if (tid == 0) {
-    for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, 1), mbar_init(empty + i, 1);
+    // TMA fills: one arrival with the transaction bytes; cp.async fills: one per producer lane
+    for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, use_tma ? 1 : 32), mbar_init(empty + i, 1);
     for (int i = 0; i < S; ++i) mbar_init(sfull + i, 1), mbar_init(sfree + i, NSW);
     mbar_init(pready + 0, NSW), mbar_init(pready + 1, NSW);
     mbar_init(pfree + 0, 1), mbar_init(pfree + 1, 1);
@@ -241,9 +246,6 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
     const int sub = lane >> 4, c = lane & 15;   // 2 key rows x 16 chunks per instruction
     const uint32_t ring_u = smem_u32(ring);
     const int nfill = sc.nfill();
-    // dense chunks starting on a 16-key boundary: TMA boxes of 16 keys (lanes 0-7 issue the two
-    // 64-element halves of one box each); otherwise 16-byte cp.async of every row
-    const bool use_tma = p.tma && p.dense && ((it.dense_lo + kb) & 15) == 0;
     for (int f = 0; f < nfill; ++f) {
       const int s = f % NSLOT;
       int t;
@@ -277,9 +279,7 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
           const int slot = __shfl_sync(0xffffffffu, sl[kk >> 4], i & 31);
           cp_async16(dst0 + i * 128 + (((c & 7) ^ (i & 7)) << 4), base + (int64_t)slot * row_stride, pol);
         }
-        cp_async_mbar_arrive_inc(full + s);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(full + s);
+        cp_async_mbar_arrive(full + s);
       }
       if (f == nt - 1) {
         if (lane == 0) TRACE(11, gtime());

@@ -13,7 +13,7 @@ from paper_2512_01278_b200.model import make_items
 from paper_2512_01278_b200.paged import PagedKvPool
 
 dev = torch.device("cuda")
-d, Hkv, G, n, t, b = 128, 2, 4, 700, 5, 2
+d, Hkv, G, n, t, b = 128, 4, 4, 300, 5, 1
 Hq = Hkv * G
 pool = PagedKvPool(1, Hkv, d, 2 * 48, 16, b, 48, torch.bfloat16, dev)
 for r in range(b):

@@ -70,7 +70,7 @@ def parse():
     p.add_argument("--k", type=int, default=4)
     p.add_argument("--sparsity", type=float, default=0.05)
     p.add_argument("--layers", type=int, default=C1["layers"])
-    p.add_argument("--variants", default="planted,sweep",
+    p.add_argument("--variants", default="planted,sweep,c3",
                    help="comma list of extra variants: planted (alpha ~ 1), sweep (s = 1/2/10%%), c3 (configs[3] "
                         "32B-shaped), none")
     p.add_argument("--pool", choices=["full", "window"], default="full")
@@ -556,8 +556,10 @@ def main():
                 variants[name]["ms_per_step"] = v["dev_s_max"] / max(3, args.steps // 2) * 1000.0
             if v.get("verify_ms_total"):
                 variants[name]["verify_gbs"] = v["verify_bytes"] / (v["verify_ms_total"] / 1000.0) / 1e9
+                variants[name]["verify_frac"] = variants[name]["verify_gbs"] / hbm
             if v.get("draft_ms_total"):
                 variants[name]["draft_gbs"] = v["draft_bytes"] / (v["draft_ms_total"] / 1000.0) / 1e9
+                variants[name]["draft_frac"] = variants[name]["draft_gbs"] / hbm
         job = m["global_batch"]
         if args.gpus > 1:
             workload = (f"configs[2]: Qwen3-8B-shaped (L={args.layers}, Hq=32, Hkv=8, d=128, V=151936) random-init "

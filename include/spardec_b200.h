@@ -231,6 +231,12 @@ int sd_forward_layers(const sd_layer_weights* weights, int32_t layers, float* x,
                       int32_t num_planted, float planted_bonus, float scale, float eps, void* workspace,
                       int64_t workspace_bytes, void* const* attn_events, int32_t flags, void* stream);
 
+/* One linear layer on the library's tuned cuBLASLt path (the LM head, model.py:339):
+ * C[R][N] (+)= A[R][K] . W^T with A, W bf16 (W [N][K], nn.Linear layout), C fp32 when
+ * c_f32 else bf16, beta 0 (overwrite) or 1 (accumulate). */
+int sd_linear(const void* A, const void* W, void* C, int32_t R, int32_t N, int32_t K, int32_t c_f32, float beta,
+              void* stream);
+
 /* Workspace sd_forward_layers needs: the attention launches' (sd_attention_workspace_bytes,
  * max over the launches) plus a RoPE cos/sin table of `rows` rows kept at its end. */
 int64_t sd_forward_workspace_bytes(int32_t rows, int32_t head_dim, int64_t attention_bytes);

@@ -170,5 +170,20 @@ def rmsnorm_cast(x: torch.Tensor, out: torch.Tensor, eps: float = 1e-6) -> torch
     return out
 
 
+def linear(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor, accumulate: bool = False) -> torch.Tensor:
+    """out (+)= a . w^T on the library's tuned cuBLASLt path (a, w bf16 contiguous, w [N][K];
+    out fp32 or bf16 [R][N])."""
+    if a.dtype != torch.bfloat16 or w.dtype != torch.bfloat16 or not (a.is_contiguous() and w.is_contiguous()
+                                                                      and out.is_contiguous()):
+        raise ContractError("linear: contiguous bf16 a and w required")
+    R, Kd = a.shape
+    if w.shape[1] != Kd or tuple(out.shape) != (R, w.shape[0]):
+        raise ContractError("linear: shape mismatch")
+    N.check(N.lib().sd_linear(a.data_ptr(), w.data_ptr(), out.data_ptr(), R, w.shape[0], Kd,
+                              1 if out.dtype == torch.float32 else 0, 1.0 if accumulate else 0.0,
+                              N.stream_handle()), "sd_linear")
+    return out
+
+
 def launch_count() -> int:
     return int(N.lib().sd_launch_count())

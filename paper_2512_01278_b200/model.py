@@ -390,6 +390,9 @@ def _forward_native(model: ToyModel, pool: PagedKvPool, tokens, row_table, row_p
 def lm_head(model: ToyModel, x: torch.Tensor) -> torch.Tensor:
     """logits = E . rmsnorm(x) (model.py:339), fp32 output."""
     hn = K.rmsnorm_cast(x.contiguous(), torch.empty(x.shape, dtype=model.dtype, device=x.device), RMS_EPS)
+    if model.dtype == torch.bfloat16 and model.embedding.is_contiguous():
+        out = torch.empty(hn.shape[0], model.embedding.shape[0], dtype=torch.float32, device=x.device)
+        return K.linear(hn, model.embedding, out)   # tuned cuBLASLt path (csrc/forward.cu)
     return _mm(hn, model.embedding.t(), True)
 
 

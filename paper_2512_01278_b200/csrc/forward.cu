@@ -258,7 +258,7 @@ int attn_launch(const sd_attn_launch& a, const void* q, void* ctx, const sd_page
 }  // namespace
 
 extern "C" int64_t sd_forward_workspace_bytes(int32_t rows, int32_t head_dim, int64_t attention_bytes) {
-  return ((attention_bytes + 255) / 256) * 256 + sd::rope_table_bytes(rows, head_dim);
+  return ((attention_bytes + 255) / 256) * 256 + sd::rope_table_bytes(rows, head_dim) + 256;  // + alignment slack
 }
 
 extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, float* x, void* hn, void* qkv, void* q,
@@ -280,12 +280,15 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
   // RoPE cos/sin of every row once for all layers, at the end of the workspace
   // (sd_forward_workspace_bytes); the attention launches get the rest
   const int64_t table_bytes = sd::rope_table_bytes(rows, kv->head_dim);
+  // the table's start is 256-byte aligned (the K5 kernel reads it in 16-byte vectors)
+  const uintptr_t ws0 = reinterpret_cast<uintptr_t>(workspace);
+  const uintptr_t tab0 = workspace != nullptr ? ((ws0 + workspace_bytes - table_bytes) & ~uintptr_t(255)) : 0;
   const bool use_table = kv->head_dim % 16 == 0 && (qkv_w % 8) == 0 && workspace != nullptr &&
-                         workspace_bytes >= table_bytes;
+                         workspace_bytes >= table_bytes + 256 && tab0 >= ws0;
   float2* table = nullptr;
   if (use_table) {
-    workspace_bytes -= table_bytes;
-    table = reinterpret_cast<float2*>(static_cast<char*>(workspace) + workspace_bytes);
+    workspace_bytes = (int64_t)(tab0 - ws0);
+    table = reinterpret_cast<float2*>(tab0);
     sd::rope_table(row_pos, rows, kv->head_dim, table, s);
   }
   // two attention launches (verify + draft) overlap on priority streams unless timed per

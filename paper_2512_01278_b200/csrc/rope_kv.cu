@@ -83,26 +83,40 @@ __global__ void rope_table_kernel(const int32_t* __restrict__ row_pos, int rows,
 
 // bf16 K5 with the precomputed table: 8 bf16 pairs (16 B of each half) per thread, rows
 // spread over the grid so every thread has work
-__global__ void __launch_bounds__(128) rope_kv_table_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t row_stride,
+// one CTA per row, one thread per 8-element group of a head half: the q / k groups are
+// rotated with the row's cos/sin (two 16-byte table loads per 4 pairs), the v row is copied;
+// the block-table lookup (only the k and v stores need it) overlaps the loads
+__global__ void __launch_bounds__(320) rope_kv_table_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t row_stride,
                                                             const int32_t* __restrict__ row_table,
                                                             const int32_t* __restrict__ row_pos, PagedKv kv, int layer,
                                                             int q_heads, const float2* __restrict__ table,
                                                             __nv_bfloat16* __restrict__ q_out) {
   const int r = blockIdx.x;
   const int D = kv.head_dim, half = D / 2, Hkv = kv.kv_heads;
-  const int pos = row_pos[r];
-  const int64_t slot = kv.slot_of(row_table[r], pos);
   const __nv_bfloat16* x = qkv + (int64_t)r * row_stride;
-  __nv_bfloat16* K = static_cast<__nv_bfloat16*>(const_cast<void*>(kv.k)) + (int64_t)layer * kv.layer_stride;
-  __nv_bfloat16* V = static_cast<__nv_bfloat16*>(const_cast<void*>(kv.v)) + (int64_t)layer * kv.layer_stride;
-  const float2* tr = table + (int64_t)r * half;
   const int vec_per_head = half / 8;                    // 8-element groups per half
   const int groups = (q_heads + Hkv) * vec_per_head;
-  for (int gi = threadIdx.x; gi < groups; gi += blockDim.x) {
+  const int vgroups = Hkv * D / 8;                      // 16-byte pieces of the v row
+  const int table_row = row_table[r];
+  const int pos = row_pos[r];
+  const int64_t slot = (kv.slot_of(table_row, pos));
+  __nv_bfloat16* K = static_cast<__nv_bfloat16*>(const_cast<void*>(kv.k)) + (int64_t)layer * kv.layer_stride;
+  __nv_bfloat16* V = static_cast<__nv_bfloat16*>(const_cast<void*>(kv.v)) + (int64_t)layer * kv.layer_stride;
+  const float4* tr = reinterpret_cast<const float4*>(table + (int64_t)r * half);
+  for (int gi = threadIdx.x; gi < groups + vgroups; gi += blockDim.x) {
+    if (gi >= groups) {  // v: plain copy into the paged slot
+      const int j = gi - groups;
+      reinterpret_cast<uint4*>(V + kv.row_off(slot, 0))[j] = reinterpret_cast<const uint4*>(x + (q_heads + Hkv) * D)[j];
+      continue;
+    }
     const int hq = gi / vec_per_head, i0 = (gi - hq * vec_per_head) * 8;
     const __nv_bfloat16* src = x + hq * D;
     const uint4 lo_raw = *reinterpret_cast<const uint4*>(src + i0);
     const uint4 hi_raw = *reinterpret_cast<const uint4*>(src + half + i0);
+    float4 cs4[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cs4[j] = __ldg(tr + i0 / 2 + j);  // (cos, sin) of pairs i0 .. i0 + 7
+    const float2* cs = reinterpret_cast<const float2*>(cs4);
     const __nv_bfloat16* lo = reinterpret_cast<const __nv_bfloat16*>(&lo_raw);
     const __nv_bfloat16* hi = reinterpret_cast<const __nv_bfloat16*>(&hi_raw);
     uint4 olo_raw, ohi_raw;
@@ -110,18 +124,14 @@ __global__ void __launch_bounds__(128) rope_kv_table_kernel(const __nv_bfloat16*
     __nv_bfloat16* ohi = reinterpret_cast<__nv_bfloat16*>(&ohi_raw);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float2 cs = tr[i0 + j];
       const float a = __bfloat162float(lo[j]), b = __bfloat162float(hi[j]);
-      olo[j] = __float2bfloat16_rn(a * cs.x - b * cs.y);
-      ohi[j] = __float2bfloat16_rn(a * cs.y + b * cs.x);
+      olo[j] = __float2bfloat16_rn(a * cs[j].x - b * cs[j].y);
+      ohi[j] = __float2bfloat16_rn(a * cs[j].y + b * cs[j].x);
     }
     __nv_bfloat16* dst = hq < q_heads ? q_out + ((int64_t)r * q_heads + hq) * D : K + kv.row_off(slot, hq - q_heads);
     *reinterpret_cast<uint4*>(dst + i0) = olo_raw;
     *reinterpret_cast<uint4*>(dst + half + i0) = ohi_raw;
   }
-  const uint4* vsrc = reinterpret_cast<const uint4*>(x + (q_heads + Hkv) * D);
-  uint4* vdst = reinterpret_cast<uint4*>(V + kv.row_off(slot, 0));
-  for (int j = threadIdx.x; j < Hkv * D / 8; j += blockDim.x) vdst[j] = vsrc[j];
 }
 
 int rope_table(const int32_t* row_pos, int rows, int head_dim, float2* table, cudaStream_t s) {
@@ -138,7 +148,7 @@ int rope_kv_write_table(const void* qkv, int64_t qkv_row_stride, int rows, const
                         const int32_t* row_pos, const sd_paged_kv* kv, int layer, int q_heads, const float2* table,
                         void* q_out, cudaStream_t s) {
   PagedKv p = make_paged(kv);
-  rope_kv_table_kernel<<<rows, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(qkv), qkv_row_stride, row_table,
+  rope_kv_table_kernel<<<rows, 320, 0, s>>>(static_cast<const __nv_bfloat16*>(qkv), qkv_row_stride, row_table,
                                             row_pos, p, layer, q_heads, table, static_cast<__nv_bfloat16*>(q_out));
   count_launch();
   return 0;

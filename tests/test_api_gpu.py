@@ -142,7 +142,8 @@ def test_bf16_mode_runs_and_is_lossless_vs_own_greedy():
     prompt = O.synthetic_prompt(0, 1, 64, 512)
     committed, stats = E.decode_to_completion(model, E.DecodeRequest(0, prompt, 48), 4, 0.25)
     assert len(committed) == 48
-    assert stats.realized_alpha > 0.5
+    assert committed == E.greedy_decode(model, prompt, 48)
+    assert stats.realized_alpha > 0.5, stats.realized_alpha
 
 
 @pytest.mark.parametrize("planted", [None, [2, 40, 77]])

@@ -153,6 +153,7 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
   uint64_t* pready = sfree + S;          // [2] P^T buffer written
   uint64_t* pfree = pready + 2;          // [2] P^T buffer consumed by the PV MMA
   uint64_t* obar = pfree + 2;            // O^T complete
+  uint64_t* qbar = obar + 1;             // the Q tile is in shared memory (softmax warps wrote it)
   float* wm = reinterpret_cast<float*>(smem + L.wm);
   float* wl = reinterpret_cast<float*>(smem + L.wl);
   float* xm = reinterpret_cast<float*>(smem + L.xm);
@@ -173,23 +174,20 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
     mbar_init(pready + 0, NSW), mbar_init(pready + 1, NSW);
     mbar_init(pfree + 0, 1), mbar_init(pfree + 1, 1);
     mbar_init(obar, 1);
+    mbar_init(qbar, NSW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // key positions and their physical slots for the whole chunk (the producer's copy loop
   // then never waits on a block-table load); keys past the chunk copy the last valid row
-  // (finite data, masked out of the softmax).  Dense items stage only the page ids.
+  // (finite data, masked out of the softmax).  Dense items stage only the page ids, and the
+  // producer warp does that itself after the CTA barrier (its first TMA boxes do not wait
+  // for the Q tile, which the softmax warps load meanwhile).
   const int32_t* trow = p.kv.table + (int64_t)it.table_row * p.kv.table_stride;
   const int pshift = p.kv.page_shift, pmask = (1 << pshift) - 1;
   const int dpos0 = it.dense_lo + kb;          // dense: position of chunk key 0
   const int dpage0 = dpos0 >> pshift;
   int32_t* spage = spos;                       // dense: [page - dpage0] -> physical page
-  if (p.dense) {
-    if (nk > 0) {
-      const int lastpg = (it.dense_lo + ke - 1) >> pshift;
-      const int npg = ((dpos0 + nt * TK - 1) >> pshift) - dpage0 + 1;
-      for (int i = tid; i < npg; i += NT) spage[i] = __ldg(trow + min(dpage0 + i, lastpg));
-    }
-  } else {
+  if (!p.dense) {
     const int nkeys = nt * TK;
     for (int j0 = 0; j0 < nkeys; j0 += 8 * NT) {  // 8 independent loads in flight per thread
       int pos[8], pg[8];
@@ -217,20 +215,29 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
     const int pos = it.dense_lo + min(kb + j, ke - 1);
     return (spage[(pos >> pshift) - dpage0] << pshift) | (pos & pmask);
   };
-  // Q rows (token-major: r = tok*G + g) -> [dhalf][NR][128 B] SWIZZLE_128B, zero padding rows
-  for (int i = tid; i < NR * 16; i += NT) {
-    const int r = i >> 4, c = i & 15;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < R)
-      v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)(it.q_row0 + r / G) * p.q_heads + h * G + r % G) * D +
-                                          c * 8);
-    *reinterpret_cast<uint4*>(qs + (c >> 3) * (NR * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
-  }
-  fence_proxy_async();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tptr;
+  if (warp < NSW) {
+    // Q rows (token-major: r = tok*G + g) -> [dhalf][NR][128 B] SWIZZLE_128B, zero padding rows
+    for (int i = tid; i < NR * 16; i += NSW * 32) {
+      const int r = i >> 4, c = i & 15;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < R)
+        v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)(it.q_row0 + r / G) * p.q_heads + h * G + r % G) * D +
+                                            c * 8);
+      *reinterpret_cast<uint4*>(qs + (c >> 3) * (NR * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(qbar);
+  } else if (warp == WPROD && p.dense && nk > 0) {
+    const int lastpg = (it.dense_lo + ke - 1) >> pshift;
+    const int npg = ((dpos0 + nt * TK - 1) >> pshift) - dpage0 + 1;
+    for (int i = lane; i < npg; i += 32) spage[i] = __ldg(trow + min(dpage0 + i, lastpg));
+    __syncwarp();
+  }
   if (tid == 0) TRACE(1, gtime());
   // barrier 0 (C > 1): every peer of the cluster has started before anyone touches its shared
   // memory (the statistics push below); arrived here, waited right before the first DSMEM use
@@ -311,6 +318,7 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
     const uint32_t id_pv = idesc_bf16(NR, true, true);
     const bool leader = lane == 0;
     int f = 0;
+    mbar_wait(qbar, 0);
     // S^T of one tile into TMEM slot `slot` (its use-th occupant) from the next ring fill
     auto qk = [&](int slot, int use) {
       const int s = f % NSLOT;

@@ -226,7 +226,7 @@ __host__ __device__ inline Layout make_layout(int NR, int NSLOT, int S, int ct, 
   L.pos = o;   o += dense ? (ct * TK / 16 + 2) * 4 : ct * TK * 4;
   L.slot = o;  o += dense ? 0 : ct * TK * 4;
   o = align_up(o, 8);
-  L.bar = o;   o += (2 * NSLOT + 2 * S + 5) * 8;
+  L.bar = o;   o += (2 * NSLOT + 2 * S + 6) * 8;
   L.wm = o;    o += NSW * NR * 4;
   L.wl = o;    o += NSW * NR * 4;
   L.xm = o;    o += 16 * NR * 4;          // [source CTA][row] pushed by every cluster peer

@@ -574,3 +574,27 @@ def test_rope_kv_write_bf16_matches_oracle():
         assert np.abs(q_out[r].double().cpu().numpy() - want_q).max() <= 1e-2 * max(1.0, np.abs(want_q).max())
         assert np.abs(kk[0, 1].double().cpu().numpy() - want_k).max() <= 1e-2 * max(1.0, np.abs(want_k).max())
         assert np.array_equal(vv[0, 1].double().cpu().numpy(), want_v)
+
+
+@pytest.mark.parametrize("R", [1, 37, 228])
+@pytest.mark.parametrize("N,Kd", [(512, 256), (4096, 4096), (8192, 4096)])
+def test_linear_tuned_cublaslt_matches_fp32(R, N, Kd):
+    """sd_linear (the tuned cuBLASLt path of the layer loop and the LM head, model.py:326-339)
+    vs a torch fp32 matmul of the same bf16 inputs: bf16 / fp32 outputs, overwrite / accumulate."""
+    g = torch.Generator(device=DEV)
+    g.manual_seed(R + N + Kd)
+    a = (torch.randn(R, Kd, device=DEV, generator=g) * 0.5).to(torch.bfloat16)
+    w = (torch.randn(N, Kd, device=DEV, generator=g) * 0.05).to(torch.bfloat16)
+    ref = a.float() @ w.float().t()
+    out = torch.empty(R, N, dtype=torch.float32, device=DEV)
+    K.linear(a, w, out)
+    x0 = torch.randn(R, N, device=DEV, generator=g)
+    x = x0.clone()
+    K.linear(a, w, x, accumulate=True)
+    ob = torch.empty(R, N, dtype=torch.bfloat16, device=DEV)
+    K.linear(a, w, ob)
+    torch.cuda.synchronize()
+    scale = ref.abs().max().item()
+    assert (out - ref).abs().max().item() <= 1e-3 * scale + 1e-4
+    assert (x - (x0 + ref)).abs().max().item() <= 1e-3 * scale + 1e-4
+    assert (ob.float() - ref).abs().max().item() <= 1e-2 * scale + 1e-3

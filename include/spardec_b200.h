@@ -231,6 +231,17 @@ int sd_forward_layers(const sd_layer_weights* weights, int32_t layers, float* x,
                       int32_t num_planted, float planted_bonus, float scale, float eps, void* workspace,
                       int64_t workspace_bytes, void* const* attn_events, int32_t flags, void* stream);
 
+/* f3: ONE launch for a layer's verify items (dense; score emission as in sd_attention) and
+ * draft items (critical list + fresh tail, one query token, no score row): the verify
+ * grid's CTAs claim the draft units (item, group of four kv heads) once their verify chunk
+ * is done, so the drafts fill the verify launch's tail on chip.  Same buffers and work-item
+ * format as two sd_attention calls; returns 1 without launching when the pair does not
+ * qualify (bf16, head_dim 128, GQA 4/8, kv_heads % 4 == 0, <= 48 verify rows per item,
+ * critical lists that stay TMEM-resident), 0 on success, else a CUDA error. */
+int sd_attention_pair(const void* q, void* out, const sd_paged_kv* kv, int32_t layer, const sd_attn_launch* verify,
+                      const sd_attn_launch* draft, const int32_t* planted, int32_t num_planted, float planted_bonus,
+                      int32_t q_heads, float scale, void* stream);
+
 /* One linear layer on the library's tuned cuBLASLt path (the LM head, model.py:339):
  * C[R][N] (+)= A[R][K] . W^T with A, W bf16 (W [N][K], nn.Linear layout), C fp32 when
  * c_f32 else bf16, beta 0 (overwrite) or 1 (accumulate). */

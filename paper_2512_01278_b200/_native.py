@@ -67,6 +67,9 @@ SIGNATURES = {
     "sd_greedy_accept": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i32, _c_p, _c_p, _c_p]),
     "sd_forward_workspace_bytes": (ctypes.c_int64, [_i32, _i32, ctypes.c_int64]),
     "sd_linear": (ctypes.c_int, [_c_p, _c_p, _c_p, _i32, _i32, _i32, _i32, ctypes.c_float, _c_p]),
+    "sd_attention_pair": (ctypes.c_int, [_c_p, _c_p, ctypes.POINTER(PagedKvDesc), _i32, ctypes.POINTER(AttnLaunchDesc),
+                                         ctypes.POINTER(AttnLaunchDesc), _c_p, _i32, ctypes.c_float, _i32,
+                                         ctypes.c_float, _c_p]),
     "sd_step_prepare": (ctypes.c_int, [_c_p, _i32, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                                        _c_p, ctypes.c_int64, _c_p]),
     "sd_step_commit": (ctypes.c_int, [_c_p, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),

@@ -3,6 +3,7 @@
 // the launch planner that picks the cluster split.
 #include "attn_umma.cuh"
 
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <algorithm>
@@ -12,382 +13,6 @@
 
 namespace sd {
 namespace umma_attn {
-
-// Fill order of the head-packed kernel's producer ring (each fill = one 32 KB K or V tile):
-//   K[0..nt), V[nt-TR..nt) over the TMEM-resident tiles, then (K[j], V[j]) j < nt-TR
-__device__ __forceinline__ void fill_tile_hp(int f, int nt, int TR, int& t, bool& isv) {
-  if (f < nt) {
-    t = f, isv = false;
-  } else if (f < nt + TR) {
-    t = nt - TR + (f - nt), isv = true;
-  } else {
-    const int g = f - nt - TR;
-    t = g >> 1, isv = g & 1;
-  }
-}
-
-// ---------------------------------------------------------------------------------------
-// Head-packed draft kernel (K1, one query token per item): a CTA covers HPC kv heads of one
-// item, and a 128-row UMMA tile is KPT = 128 / HPC keys x HPC heads (head-major rows), so
-//   S^T[(head, key)][HPC*G] = K_rows . Q^T      (only the row's own head block is used)
-//   O^T[d][HPC*G]         += V_rows^T . P^T    (P^T is block-diagonal: exact per head)
-// Every statistic of a (head, q head) row lives inside one warp (KPT = 32 or 16 keys of the
-// tile per head), so there is no CTA exchange; the setup cost is paid once per HPC heads
-// and every fill moves 32 KB however small the critical set is.
-template <int N>
-__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, float* v) {
-  if constexpr (N == 4) {
-    uint32_t r0, r1, r2, r3;
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(taddr) : "memory");
-    v[0] = __uint_as_float(r0), v[1] = __uint_as_float(r1), v[2] = __uint_as_float(r2), v[3] = __uint_as_float(r3);
-  } else if constexpr (N == 8) {
-    uint32_t r[8];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr) : "memory");
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
-  } else {
-    static_assert(N % 16 == 0, "tcgen05.ld width");
-#pragma unroll
-    for (int c = 0; c < N; c += 16) tmem_ld16(taddr + c, v + c);
-  }
-}
-
-// shared-memory layout of the head-packed kernel: no cross-warp statistics arrays
-__host__ __device__ inline Layout make_hp_layout(int NR, int NSLOT, int TMAX, int ct) {
-  Layout L{};
-  int o = 0;
-  L.ring = o;  o += NSLOT * TILE_BYTES;
-  L.q = o;     o += 2 * NR * 128;
-  L.pbuf = o;  o += 2 * NR * TK * 2;
-  L.pos = o;   o += ct * TK * 4;
-  L.slot = o;  o += ct * TK * 4;
-  o = align_up(o, 8);
-  L.bar = o;   o += (2 * NSLOT + 2 * TMAX + 5) * 8;
-  L.tptr = o;  o += 16;
-  L.wm = L.wl = L.xm = L.xl = L.rowlse = 0;
-  L.total = align_up(o, 128) + 1024;
-  return L;
-}
-
-// head-packed kernel warp layout: softmax warps 0-3, HP_NPROD producer warps, the MMA warp
-constexpr int HP_NPROD = 4;
-constexpr int HP_WPROD = NSW, HP_WMMA = NSW + HP_NPROD;
-constexpr int HP_NT = (NSW + HP_NPROD + 1) * 32;
-
-template <int G, int HPC, int NSLOT, int TCOLS>
-__device__ __forceinline__ void draft_body(const Params& p, const int hgroup, const int item_idx) {
-  constexpr int NQ = HPC * G;                       // q heads of the CTA
-  constexpr int NR = NQ < 16 ? 16 : NQ;             // UMMA N
-  constexpr int KPT = TK / HPC;                     // keys per tile
-  constexpr int TMAX = (TCOLS - NR) / NR;
-  constexpr int OCOL = TMAX * NR;
-  constexpr int WH = KPT >= 32 ? 1 : 32 / KPT;      // heads per warp (rows of a warp)
-  static_assert(KPT == 16 || KPT == 32, "head packing: 4 or 8 heads per CTA");
-
-  const int h0 = hgroup * HPC;
-  const Item it = load_item(p.items, item_idx);
-  const int nk = it.num_keys();
-  const int nt = (nk + KPT - 1) / KPT;
-  const int TR = min(nt, TMAX);
-  const int nfill = 3 * nt - TR;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int cta_lin = blockIdx.y * gridDim.x + blockIdx.x;
-#define HTRACE(k, val)                                                                                  \
-  do {                                                                                                  \
-    if (p.trace && cta_lin < kTraceCtas) p.trace[cta_lin * kTraceSlots + (k)] = (val);                  \
-  } while (0)
-  if (tid == 0) {
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    HTRACE(0, gtime());
-    HTRACE(9, (uint64_t)smid | ((uint64_t)nt << 32));
-  }
-
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const Layout L = make_hp_layout(NR, NSLOT, TMAX, (nt * KPT + TK - 1) / TK);
-  unsigned char* ring = smem + L.ring;
-  unsigned char* qs = smem + L.q;
-  unsigned char* pbuf = smem + L.pbuf;
-  int32_t* spos = reinterpret_cast<int32_t*>(smem + L.pos);
-  int32_t* sslot = reinterpret_cast<int32_t*>(smem + L.slot);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);
-  uint64_t* empty = full + NSLOT;
-  uint64_t* sfull = empty + NSLOT;
-  uint64_t* sfree = sfull + TMAX;
-  uint64_t* pready = sfree + TMAX;
-  uint64_t* pfree = pready + 2;
-  uint64_t* obar = pfree + 2;
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L.tptr);
-
-  if (warp == HP_WMMA) tmem_alloc(tptr, TCOLS);
-  if (tid == 0) {
-    for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, 32 * HP_NPROD), mbar_init(empty + i, 1);
-    for (int i = 0; i < TMAX; ++i) mbar_init(sfull + i, 1), mbar_init(sfree + i, NSW);
-    mbar_init(pready + 0, NSW), mbar_init(pready + 1, NSW);
-    mbar_init(pfree + 0, 1), mbar_init(pfree + 1, 1);
-    mbar_init(obar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  {
-    const int nkeys = nt * KPT;
-    const int32_t* trow = p.kv.table + (int64_t)it.table_row * p.kv.table_stride;
-    const int pmask = (1 << p.kv.page_shift) - 1;
-    for (int j0 = 0; j0 < nkeys; j0 += 8 * HP_NT) {
-      int pos[8], pg[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) pos[k] = it.key_pos(p.crit, min(j0 + k * HP_NT + tid, nk - 1));
-#pragma unroll
-      for (int k = 0; k < 8; ++k) pg[k] = __ldg(trow + (pos[k] >> p.kv.page_shift));
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int j = j0 + k * HP_NT + tid;
-        if (j < nkeys) {
-          spos[j] = j < nk ? pos[k] : -1;
-          sslot[j] = (pg[k] << p.kv.page_shift) | (pos[k] & pmask);
-        }
-      }
-    }
-  }
-  // Q: the CTA's NQ q heads are contiguous in the row (heads h0.. x group)
-  for (int i = tid; i < NR * 16; i += HP_NT) {
-    const int r = i >> 4, c = i & 15;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < NQ) v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)it.q_row0 * p.q_heads + h0 * G + r) * D + c * 8);
-    *reinterpret_cast<uint4*>(qs + (c >> 3) * (NR * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
-  }
-  // P^T buffers: off-diagonal blocks stay zero for the whole launch
-  for (int i = tid; i < 2 * NR * TK * 2 / 16; i += HP_NT) reinterpret_cast<uint4*>(pbuf)[i] = make_uint4(0, 0, 0, 0);
-  fence_proxy_async();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tptr;
-  if (tid == 0) HTRACE(1, gtime());
-
-  const int64_t row_stride = (int64_t)p.kv.kv_heads * D;
-  const __nv_bfloat16* Kg = static_cast<const __nv_bfloat16*>(p.kv.k) + (int64_t)p.layer * p.kv.layer_stride + h0 * D;
-  const __nv_bfloat16* Vg = static_cast<const __nv_bfloat16*>(p.kv.v) + (int64_t)p.layer * p.kv.layer_stride + h0 * D;
-
-  if (warp >= HP_WPROD && warp < HP_WPROD + HP_NPROD) {
-    // producers: warp pw copies rows [pw * 128 / HP_NPROD, ...) of every 32 KB fill (one head's keys)
-    const int pw = warp - HP_WPROD;
-    const uint64_t pol = policy_evict_first();
-    const int sub = lane >> 4, c = lane & 15;
-    const uint32_t ring_u = smem_u32(ring);
-    constexpr int KK = TK / 2 / HP_NPROD;  // row pairs per warp
-    for (int f = 0; f < nfill; ++f) {
-      const int s = f % NSLOT;
-      int t;
-      bool isv;
-      fill_tile_hp(f, nt, TR, t, isv);
-      const __nv_bfloat16* base = (isv ? Vg : Kg) + c * 8;
-      const int sl = sslot[t * KPT + (lane % KPT)];
-      if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
-      const uint32_t dst0 = ring_u + s * TILE_BYTES + (c >> 3) * (TK * 128);
-#pragma unroll
-      for (int k2 = 0; k2 < KK; ++k2) {
-        const int kk = pw * KK + k2;
-        const int i = 2 * kk + sub;            // tile row = head-major (hh, key)
-        const int hh = (2 * kk) / KPT;         // same for both rows of the instruction
-        const int slot = __shfl_sync(0xffffffffu, sl, ((2 * kk) % KPT) + sub);
-        cp_async16(dst0 + i * 128 + (((c & 7) ^ (i & 7)) << 4), base + (int64_t)slot * row_stride + hh * D, pol);
-      }
-      cp_async_mbar_arrive(full + s);
-    }
-    if (pw == 0 && lane == 0) HTRACE(7, gtime());
-    return;
-  }
-
-  if (warp == HP_WMMA) {
-    const uint32_t ring_u = smem_u32(ring), q_u = smem_u32(qs), p_u = smem_u32(pbuf);
-    const uint32_t id_qk = idesc_bf16(NR, false, false);
-    const uint32_t id_pv = idesc_bf16(NR, true, true);
-    const bool leader = lane == 0;
-    int f = 0;
-    auto qk = [&](int u, int s) {
-      mbar_wait(full + s, (f / NSLOT) & 1);
-      if (u >= TMAX) mbar_wait(sfree + u % TMAX, ((u / TMAX) - 1) & 1);
-      fence_proxy_async();
-      tc_fence_after();
-      if (leader) {
-        const uint32_t a0 = ring_u + s * TILE_BYTES;
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off = (ks & 3) << 5;
-          const uint64_t a = smem_desc(a0 + (ks >> 2) * (TK * 128) + off, 16, 1024, 2);
-          const uint64_t b = smem_desc(q_u + (ks >> 2) * (NR * 128) + off, 16, 1024, 2);
-          umma(tbase + (u % TMAX) * NR, a, b, id_qk, ks > 0);
-        }
-        umma_commit(empty + s);
-        umma_commit(sfull + u % TMAX);
-      }
-      __syncwarp();
-      ++f;
-    };
-    for (int t = 0; t < nt; ++t) qk(t, f % NSLOT);
-    for (int i2 = 0; i2 < nt; ++i2) {
-      if (i2 >= TR) qk(nt + (i2 - TR), f % NSLOT);
-      const int s = f % NSLOT;
-      mbar_wait(full + s, (f / NSLOT) & 1);
-      mbar_wait(pready + (i2 & 1), (i2 >> 1) & 1);
-      fence_proxy_async();
-      tc_fence_after();
-      if (leader) {
-        const uint32_t a0 = ring_u + s * TILE_BYTES;
-        const uint32_t b0 = p_u + (i2 & 1) * (NR * TK * 2);
-#pragma unroll
-        for (int ks = 0; ks < TK / 16; ++ks) {
-          const uint64_t a = smem_desc(a0 + ks * 16 * 128, TK * 128, 1024, 2);
-          const uint64_t b = smem_desc(b0 + ks * 2 * 128, 128, TK * 16, 0);
-          umma(tbase + OCOL, a, b, id_pv, (i2 > 0 || ks > 0) ? 1u : 0u);
-        }
-        umma_commit(empty + s);
-        umma_commit(pfree + (i2 & 1));
-        if (i2 == nt - 1) umma_commit(obar);
-      }
-      __syncwarp();
-      ++f;
-    }
-    asm volatile("bar.sync 2, %0;\n" ::"n"((NSW + 1) * 32) : "memory");
-    tc_fence_after();
-    tmem_dealloc(tbase, TCOLS);
-    return;
-  }
-
-  // ===================== softmax warps: thread = (head, key) row of the tile =====================
-  const int row = warp * 32 + lane;
-  const int hh = row / KPT, k = row % KPT;
-  const int hsel = WH > 1 ? (lane / KPT) : 0;            // which of the warp's heads
-  const int col0 = (warp * 32 / KPT) * G;                // first S column the warp reads
-  const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
-  float m[G], l[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) m[g] = -INFINITY, l[g] = 0.f;
-
-  auto load_s = [&](int u, float (&v)[G]) {
-    float w[WH * G];
-    tmem_ld_n<WH * G>(tl + (u % TMAX) * NR + col0, w);
-    tmem_wait_ld();
-#pragma unroll
-    for (int g = 0; g < G; ++g) v[g] = WH > 1 && hsel ? w[G + g] : w[g];
-  };
-  auto key_info = [&](int t, int& pos, float& bias, bool& vis) {
-    const int j = t * KPT + k;
-    pos = spos[j];
-    vis = pos >= 0 && (j < it.crit_len || pos <= it.qpos0);
-    bias = (vis && p.n_planted) ? planted_bias(p.planted, p.n_planted, p.bonus_log2, pos) : 0.f;
-  };
-  auto release = [&](int u) {
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(sfree + u % TMAX);
-  };
-
-  for (int t = 0; t < nt; ++t) {
-    int pos;
-    float bias;
-    bool vis;
-    key_info(t, pos, bias, vis);
-    mbar_wait(sfull + t % TMAX, (t / TMAX) & 1);
-    tc_fence_after();
-    float v[G];
-    load_s(t, v);
-    if (t < nt - TR) release(t);
-    if (vis) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float s2 = fmaf(v[g], p.scale_log2, bias);
-        const float nm = fmaxf(m[g], s2);
-        l[g] = l[g] * ex2(m[g] - nm) + ex2(s2 - nm);
-        m[g] = nm;
-      }
-    }
-  }
-  // statistics of each (head, q head) row: reduce over the KPT lanes of this head
-  float lse[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-#pragma unroll
-    for (int o = KPT / 2; o >= 1; o >>= 1) {
-      const float om = __shfl_xor_sync(0xffffffffu, m[g], o), ol = __shfl_xor_sync(0xffffffffu, l[g], o);
-      stat_merge(m[g], l[g], om, ol);
-    }
-    lse[g] = m[g] + log2f(l[g]);
-  }
-  if (tid == 0) {
-    HTRACE(2, gtime());
-    HTRACE(3, gtime());
-  }
-
-  const bool scores = p.acc != nullptr && it.acc_row >= 0;
-  for (int i2 = 0; i2 < nt; ++i2) {
-    const int t = i2 < TR ? nt - TR + i2 : i2 - TR;
-    const int u = i2 < TR ? t : nt + t;
-    int pos;
-    float bias;
-    bool vis;
-    key_info(t, pos, bias, vis);
-    mbar_wait(sfull + u % TMAX, (u / TMAX) & 1);
-    tc_fence_after();
-    float v[G];
-    load_s(u, v);
-    release(u);
-    float sum = 0.f;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      v[g] = vis ? ex2(fmaf(v[g], p.scale_log2, bias) - lse[g]) : 0.f;
-      sum += v[g];
-    }
-    if (scores && sum != 0.f) red_add_fx(p.acc + (int64_t)it.acc_row * p.acc_stride + pos, sum, p.acc_scale);
-    if (i2 >= 2) mbar_wait(pfree + (i2 & 1), ((i2 >> 1) - 1) & 1);
-    // P^T row `row`: this head's G columns (the rest of the row stays zero)
-    unsigned char* pb = pbuf + (i2 & 1) * (NR * TK * 2) + row * 16 + ((hh * G) >> 3) * (TK * 16);
-    if constexpr (G == 8) {
-      uint4 w;
-      __nv_bfloat162 b0 = __floats2bfloat162_rn(v[0], v[1]), b1 = __floats2bfloat162_rn(v[2], v[3]);
-      __nv_bfloat162 b2 = __floats2bfloat162_rn(v[4], v[5]), b3 = __floats2bfloat162_rn(v[6], v[7]);
-      w.x = *reinterpret_cast<uint32_t*>(&b0), w.y = *reinterpret_cast<uint32_t*>(&b1);
-      w.z = *reinterpret_cast<uint32_t*>(&b2), w.w = *reinterpret_cast<uint32_t*>(&b3);
-      *reinterpret_cast<uint4*>(pb) = w;
-    } else {
-      static_assert(G == 4, "group size 4 or 8");
-      uint2 w;
-      __nv_bfloat162 b0 = __floats2bfloat162_rn(v[0], v[1]), b1 = __floats2bfloat162_rn(v[2], v[3]);
-      w.x = *reinterpret_cast<uint32_t*>(&b0), w.y = *reinterpret_cast<uint32_t*>(&b1);
-      *reinterpret_cast<uint2*>(pb + ((hh * G) & 7) * 2) = w;
-    }
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(pready + (i2 & 1));
-  }
-
-  float o[NR];
-  if (tid == 0) HTRACE(4, gtime());
-  if (nt > 0) {
-    mbar_wait(obar, 0);
-    tc_fence_after();
-    if (tid == 0) HTRACE(5, gtime());
-    tmem_ld_row<NR>(tl + OCOL, o);
-  } else {
-#pragma unroll
-    for (int r = 0; r < NR; ++r) o[r] = 0.f;
-  }
-  tc_fence_before();
-  asm volatile("bar.arrive 2, %0;\n" ::"n"((NSW + 1) * 32) : "memory");
-#pragma unroll
-  for (int r = 0; r < NQ; ++r)
-    p.out[((int64_t)it.q_row0 * p.q_heads + h0 * G + r) * D + row] = __float2bfloat16_rn(o[r]);
-  if (p.lse_out != nullptr && k == 0) {
-#pragma unroll
-    for (int g = 0; g < G; ++g) p.lse_out[(int64_t)it.q_row0 * p.q_heads + (h0 + hh) * G + g] = lse[g] * LN2;
-  }
-  if (tid == 0) HTRACE(6, gtime());
-#undef HTRACE
-}
 
 template <int G, int HPC, int NSLOT, int TCOLS>
 __global__ void __launch_bounds__(HP_NT, TCOLS == 512 ? 1 : 2) attn_umma_hp_kernel(const __grid_constant__ Params p) {
@@ -637,6 +262,73 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
                 : launch_verify_g8(prm, pl.NR, pl.C, num_items, kvp->kv_heads, stream);
 }
 
+// f3: one fused launch for a layer's verify items (dense, score emission) and draft items
+// (critical list, one query token): the verify clusters' CTAs claim the draft units once
+// their verify chunk is done (attn_fused_kernel).  Returns 1 without launching when the
+// shapes do not qualify (the caller launches the two separately), 0 on success.
+int launch_attn_pair(const void* q, void* out, const sd_paged_kv* kvp, int layer, const int32_t* v_items, int v_n,
+                     int v_keys, int v_nq, unsigned long long* v_acc, int64_t v_acc_stride, int v_acc_shift,
+                     const int32_t* d_items, int d_n, int d_keys, const int32_t* d_crit, const int32_t* planted,
+                     int n_planted, float bonus, int q_heads, float scale, cudaStream_t stream) {
+  using namespace umma_attn;
+  const int G = q_heads / kvp->kv_heads;
+  if (v_n < 1 || d_n < 1 || d_crit == nullptr || kvp->dtype != SD_DTYPE_BF16 || kvp->head_dim != D ||
+      !(G == 4 || G == 8) || kvp->kv_heads % 4 != 0 || kvp->page_shift < 4 || env_int("SD_ATTN_TRACE", 0))
+    return 1;
+  UmmaPlan pl;
+  if (!umma_plan(kvp, v_n, v_keys, v_nq, q_heads, 1, &pl) || pl.NR > kNarrowMaxNR) return 1;
+  const int NRd = 4 * G, tmax = (256 - NRd) / NRd;
+  const int ct_tiles = (max(d_keys, 1) + 31) / 32;
+  const int ct = (ct_tiles * 32 + TK - 1) / TK;
+  if (ct_tiles > tmax) return 1;
+  const int Sv = 256 / pl.NR;
+  const int smem = std::max(make_layout(pl.NR, 2, Sv, pl.chunk / TK, 1).total, make_hp_layout(NRd, 2, tmax, ct).total);
+  if (smem > 113 * 1024) return 1;
+  static std::mutex mu;
+  static unsigned long long* ctr[64] = {};
+  static std::atomic<uint32_t> tag{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (ctr[dev & 63] == nullptr) {
+      if (cudaMalloc(&ctr[dev & 63], sizeof(unsigned long long)) != cudaSuccess) return 1;
+      cudaMemset(ctr[dev & 63], 0, sizeof(unsigned long long));
+    }
+  }
+  uint32_t tg = tag.fetch_add(1) + 1;
+  if (tg == 0) tg = tag.fetch_add(1) + 1;
+  Params pv{}, pd{};
+  pv.q = pd.q = static_cast<const __nv_bfloat16*>(q);
+  pv.out = pd.out = static_cast<__nv_bfloat16*>(out);
+  pv.kv = pd.kv = make_paged(kvp);
+  pv.layer = pd.layer = layer;
+  pv.planted = pd.planted = planted;
+  pv.n_planted = pd.n_planted = n_planted;
+  pv.bonus_log2 = pd.bonus_log2 = bonus * LOG2E;
+  pv.q_heads = pd.q_heads = q_heads;
+  pv.scale_log2 = pd.scale_log2 = scale * LOG2E;
+  pv.items = v_items;
+  pv.acc = v_acc;
+  pv.acc_stride = v_acc_stride;
+  pv.acc_scale = ldexpf(1.f, v_acc_shift);
+  pv.chunk = pl.chunk;
+  pv.dense = 1;
+  static const int tma_env = env_int("SD_K2_TMA", 1);
+  if (tma_env) {
+    const int64_t loff = (int64_t)layer * kvp->layer_stride * 2;
+    pv.tma = pool_map(&pv.tmk, static_cast<const char*>(kvp->k) + loff, kvp->num_slots, kvp->kv_heads) &&
+             pool_map(&pv.tmv, static_cast<const char*>(kvp->v) + loff, kvp->num_slots, kvp->kv_heads);
+  }
+  pd.items = d_items;
+  pd.crit = d_crit;
+  pd.chunk = ct * TK;
+  FusedCtl fc{ctr[dev & 63], tg, d_n * (kvp->kv_heads / 4), kvp->kv_heads / 4};
+  const int rc = G == 4 ? launch_fused_g4(pv, pd, fc, pl.NR, pl.C, v_n, kvp->kv_heads, smem, stream)
+                        : launch_fused_g8(pv, pd, fc, pl.NR, pl.C, v_n, kvp->kv_heads, smem, stream);
+  return rc < 0 ? 1 : rc;
+}
+
 }  // namespace sd
 
 // Diagnostics: per-CTA phase timestamps of the last traced verify launch (SD_ATTN_TRACE=1):
@@ -648,4 +340,18 @@ extern "C" int sd_attention_trace_umma(uint64_t* host_dst, int32_t ctas) {
   cudaError_t e = cudaMemcpy(host_dst, sd::umma_attn::g_trace_buf, sizeof(uint64_t) * sd::umma_attn::kTraceSlots * ctas,
                              cudaMemcpyDeviceToHost);
   return e == cudaSuccess ? 0 : (int)e;
+}
+
+// f3 fused verify + draft launch through the C ABI (csrc/attn_umma.cu launch_attn_pair):
+// returns 1 when the pair does not qualify (launch the two with sd_attention instead).
+extern "C" int sd_attention_pair(const void* q, void* out, const sd_paged_kv* kv, int32_t layer,
+                                 const sd_attn_launch* verify, const sd_attn_launch* draft, const int32_t* planted,
+                                 int32_t num_planted, float planted_bonus, int32_t q_heads, float scale, void* stream) {
+  SD_REQUIRE(q != nullptr && out != nullptr && kv != nullptr && verify != nullptr && draft != nullptr,
+             "sd_attention_pair: null pointer");
+  SD_REQUIRE(kv->kv_heads > 0 && q_heads % kv->kv_heads == 0, "sd_attention_pair: kv_heads must divide q_heads");
+  return sd::launch_attn_pair(q, out, kv, layer, verify->items, verify->num_items, verify->max_keys, verify->max_nq,
+                              reinterpret_cast<unsigned long long*>(verify->acc), verify->acc_row_stride,
+                              verify->acc_shift, draft->items, draft->num_items, draft->max_keys, draft->crit, planted,
+                              num_planted, planted_bonus, q_heads, scale, static_cast<cudaStream_t>(stream));
 }

@@ -108,7 +108,7 @@ __device__ __forceinline__ void rows_reduce_store(float* m, float* l, int lane, 
 }
 
 template <int G, int NR, int NSLOT, int TCOLS>
-__device__ __forceinline__ void verify_body(const Params& p, const int h, const int item_idx) {
+__device__ __forceinline__ void verify_body(const Params& p, const int h, const int item_idx, bool relinquish = true) {
   constexpr int S = TCOLS / NR;             // logits slots (slot S-1 = O^T accumulator)
   constexpr int OCOL = (S - 1) * NR;
   constexpr int CH = col_chunk<NR>();
@@ -166,7 +166,7 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
   const bool use_tma = p.tma && p.dense && ((it.dense_lo + kb) & 15) == 0;
 
   // ---- setup ----
-  if (warp == WMMA) tmem_alloc(tptr, TCOLS);
+  if (warp == WMMA) tmem_alloc(tptr, TCOLS, relinquish);
   if (tid == 0) {
     // TMA fills: one arrival with the transaction bytes; cp.async fills: one per producer lane
     for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, use_tma ? 1 : 32), mbar_init(empty + i, 1);
@@ -606,9 +606,469 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
 #undef TRACE
 }
 
+// Fill order of the head-packed kernel's producer ring (each fill = one 32 KB K or V tile):
+//   K[0..nt), V[nt-TR..nt) over the TMEM-resident tiles, then (K[j], V[j]) j < nt-TR
+__device__ __forceinline__ void fill_tile_hp(int f, int nt, int TR, int& t, bool& isv) {
+  if (f < nt) {
+    t = f, isv = false;
+  } else if (f < nt + TR) {
+    t = nt - TR + (f - nt), isv = true;
+  } else {
+    const int g = f - nt - TR;
+    t = g >> 1, isv = g & 1;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Head-packed draft kernel (K1, one query token per item): a CTA covers HPC kv heads of one
+// item, and a 128-row UMMA tile is KPT = 128 / HPC keys x HPC heads (head-major rows), so
+//   S^T[(head, key)][HPC*G] = K_rows . Q^T      (only the row's own head block is used)
+//   O^T[d][HPC*G]         += V_rows^T . P^T    (P^T is block-diagonal: exact per head)
+// Every statistic of a (head, q head) row lives inside one warp (KPT = 32 or 16 keys of the
+// tile per head), so there is no CTA exchange; the setup cost is paid once per HPC heads
+// and every fill moves 32 KB however small the critical set is.
+template <int N>
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, float* v) {
+  if constexpr (N == 4) {
+    uint32_t r0, r1, r2, r3;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(taddr) : "memory");
+    v[0] = __uint_as_float(r0), v[1] = __uint_as_float(r1), v[2] = __uint_as_float(r2), v[3] = __uint_as_float(r3);
+  } else if constexpr (N == 8) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr) : "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+  } else {
+    static_assert(N % 16 == 0, "tcgen05.ld width");
+#pragma unroll
+    for (int c = 0; c < N; c += 16) tmem_ld16(taddr + c, v + c);
+  }
+}
+
+// shared-memory layout of the head-packed kernel: no cross-warp statistics arrays
+__host__ __device__ inline Layout make_hp_layout(int NR, int NSLOT, int TMAX, int ct) {
+  Layout L{};
+  int o = 0;
+  L.ring = o;  o += NSLOT * TILE_BYTES;
+  L.q = o;     o += 2 * NR * 128;
+  L.pbuf = o;  o += 2 * NR * TK * 2;
+  L.pos = o;   o += ct * TK * 4;
+  L.slot = o;  o += ct * TK * 4;
+  o = align_up(o, 8);
+  L.bar = o;   o += (2 * NSLOT + 2 * TMAX + 5) * 8;
+  L.tptr = o;  o += 16;
+  L.wm = L.wl = L.xm = L.xl = L.rowlse = 0;
+  L.total = align_up(o, 128) + 1024;
+  return L;
+}
+
+// head-packed kernel warp layout: softmax warps 0-3, NPROD producer warps, the MMA warp
+// (the standalone K1 kernel runs HP_NPROD = 4 producers; inside the fused verify + draft
+// kernel it runs on the verify kernel's six warps with one)
+constexpr int HP_NPROD = 4;
+constexpr int HP_NT = (NSW + HP_NPROD + 1) * 32;
+
+template <int G, int HPC, int NSLOT, int TCOLS, int NPROD = HP_NPROD>
+__device__ __forceinline__ void draft_body(const Params& p, const int hgroup, const int item_idx, bool relinquish = true) {
+  constexpr int HP_WPROD = NSW, HP_WMMA = NSW + NPROD;
+  constexpr int BNT = (NSW + NPROD + 1) * 32;
+  constexpr int NQ = HPC * G;                       // q heads of the CTA
+  constexpr int NR = NQ < 16 ? 16 : NQ;             // UMMA N
+  constexpr int KPT = TK / HPC;                     // keys per tile
+  constexpr int TMAX = (TCOLS - NR) / NR;
+  constexpr int OCOL = TMAX * NR;
+  constexpr int WH = KPT >= 32 ? 1 : 32 / KPT;      // heads per warp (rows of a warp)
+  static_assert(KPT == 16 || KPT == 32, "head packing: 4 or 8 heads per CTA");
+
+  const int h0 = hgroup * HPC;
+  const Item it = load_item(p.items, item_idx);
+  const int nk = it.num_keys();
+  const int nt = (nk + KPT - 1) / KPT;
+  const int TR = min(nt, TMAX);
+  const int nfill = 3 * nt - TR;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cta_lin = blockIdx.y * gridDim.x + blockIdx.x;
+#define HTRACE(k, val)                                                                                  \
+  do {                                                                                                  \
+    if (p.trace && cta_lin < kTraceCtas) p.trace[cta_lin * kTraceSlots + (k)] = (val);                  \
+  } while (0)
+  if (tid == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    HTRACE(0, gtime());
+    HTRACE(9, (uint64_t)smid | ((uint64_t)nt << 32));
+  }
+
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const Layout L = make_hp_layout(NR, NSLOT, TMAX, (nt * KPT + TK - 1) / TK);
+  unsigned char* ring = smem + L.ring;
+  unsigned char* qs = smem + L.q;
+  unsigned char* pbuf = smem + L.pbuf;
+  int32_t* spos = reinterpret_cast<int32_t*>(smem + L.pos);
+  int32_t* sslot = reinterpret_cast<int32_t*>(smem + L.slot);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);
+  uint64_t* empty = full + NSLOT;
+  uint64_t* sfull = empty + NSLOT;
+  uint64_t* sfree = sfull + TMAX;
+  uint64_t* pready = sfree + TMAX;
+  uint64_t* pfree = pready + 2;
+  uint64_t* obar = pfree + 2;
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L.tptr);
+
+  if (warp == HP_WMMA) tmem_alloc(tptr, TCOLS, relinquish);
+  if (tid == 0) {
+    for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, 32 * NPROD), mbar_init(empty + i, 1);
+    for (int i = 0; i < TMAX; ++i) mbar_init(sfull + i, 1), mbar_init(sfree + i, NSW);
+    mbar_init(pready + 0, NSW), mbar_init(pready + 1, NSW);
+    mbar_init(pfree + 0, 1), mbar_init(pfree + 1, 1);
+    mbar_init(obar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  {
+    const int nkeys = nt * KPT;
+    const int32_t* trow = p.kv.table + (int64_t)it.table_row * p.kv.table_stride;
+    const int pmask = (1 << p.kv.page_shift) - 1;
+    for (int j0 = 0; j0 < nkeys; j0 += 8 * BNT) {
+      int pos[8], pg[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pos[k] = it.key_pos(p.crit, min(j0 + k * BNT + tid, nk - 1));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pg[k] = __ldg(trow + (pos[k] >> p.kv.page_shift));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = j0 + k * BNT + tid;
+        if (j < nkeys) {
+          spos[j] = j < nk ? pos[k] : -1;
+          sslot[j] = (pg[k] << p.kv.page_shift) | (pos[k] & pmask);
+        }
+      }
+    }
+  }
+  // Q: the CTA's NQ q heads are contiguous in the row (heads h0.. x group)
+  for (int i = tid; i < NR * 16; i += BNT) {
+    const int r = i >> 4, c = i & 15;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < NQ) v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)it.q_row0 * p.q_heads + h0 * G + r) * D + c * 8);
+    *reinterpret_cast<uint4*>(qs + (c >> 3) * (NR * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+  }
+  // P^T buffers: off-diagonal blocks stay zero for the whole launch
+  for (int i = tid; i < 2 * NR * TK * 2 / 16; i += BNT) reinterpret_cast<uint4*>(pbuf)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tptr;
+  if (tid == 0) HTRACE(1, gtime());
+
+  const int64_t row_stride = (int64_t)p.kv.kv_heads * D;
+  const __nv_bfloat16* Kg = static_cast<const __nv_bfloat16*>(p.kv.k) + (int64_t)p.layer * p.kv.layer_stride + h0 * D;
+  const __nv_bfloat16* Vg = static_cast<const __nv_bfloat16*>(p.kv.v) + (int64_t)p.layer * p.kv.layer_stride + h0 * D;
+
+  if (warp >= HP_WPROD && warp < HP_WPROD + NPROD) {
+    // producers: warp pw copies rows [pw * 128 / NPROD, ...) of every 32 KB fill (one head's keys)
+    const int pw = warp - HP_WPROD;
+    const uint64_t pol = policy_evict_first();
+    const int sub = lane >> 4, c = lane & 15;
+    const uint32_t ring_u = smem_u32(ring);
+    constexpr int KK = TK / 2 / NPROD;  // row pairs per warp
+    for (int f = 0; f < nfill; ++f) {
+      const int s = f % NSLOT;
+      int t;
+      bool isv;
+      fill_tile_hp(f, nt, TR, t, isv);
+      const __nv_bfloat16* base = (isv ? Vg : Kg) + c * 8;
+      const int sl = sslot[t * KPT + (lane % KPT)];
+      if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
+      const uint32_t dst0 = ring_u + s * TILE_BYTES + (c >> 3) * (TK * 128);
+#pragma unroll
+      for (int k2 = 0; k2 < KK; ++k2) {
+        const int kk = pw * KK + k2;
+        const int i = 2 * kk + sub;            // tile row = head-major (hh, key)
+        const int hh = (2 * kk) / KPT;         // same for both rows of the instruction
+        const int slot = __shfl_sync(0xffffffffu, sl, ((2 * kk) % KPT) + sub);
+        cp_async16(dst0 + i * 128 + (((c & 7) ^ (i & 7)) << 4), base + (int64_t)slot * row_stride + hh * D, pol);
+      }
+      cp_async_mbar_arrive(full + s);
+    }
+    if (pw == 0 && lane == 0) HTRACE(7, gtime());
+    return;
+  }
+
+  if (warp == HP_WMMA) {
+    const uint32_t ring_u = smem_u32(ring), q_u = smem_u32(qs), p_u = smem_u32(pbuf);
+    const uint32_t id_qk = idesc_bf16(NR, false, false);
+    const uint32_t id_pv = idesc_bf16(NR, true, true);
+    const bool leader = lane == 0;
+    int f = 0;
+    auto qk = [&](int u, int s) {
+      mbar_wait(full + s, (f / NSLOT) & 1);
+      if (u >= TMAX) mbar_wait(sfree + u % TMAX, ((u / TMAX) - 1) & 1);
+      fence_proxy_async();
+      tc_fence_after();
+      if (leader) {
+        const uint32_t a0 = ring_u + s * TILE_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t off = (ks & 3) << 5;
+          const uint64_t a = smem_desc(a0 + (ks >> 2) * (TK * 128) + off, 16, 1024, 2);
+          const uint64_t b = smem_desc(q_u + (ks >> 2) * (NR * 128) + off, 16, 1024, 2);
+          umma(tbase + (u % TMAX) * NR, a, b, id_qk, ks > 0);
+        }
+        umma_commit(empty + s);
+        umma_commit(sfull + u % TMAX);
+      }
+      __syncwarp();
+      ++f;
+    };
+    for (int t = 0; t < nt; ++t) qk(t, f % NSLOT);
+    for (int i2 = 0; i2 < nt; ++i2) {
+      if (i2 >= TR) qk(nt + (i2 - TR), f % NSLOT);
+      const int s = f % NSLOT;
+      mbar_wait(full + s, (f / NSLOT) & 1);
+      mbar_wait(pready + (i2 & 1), (i2 >> 1) & 1);
+      fence_proxy_async();
+      tc_fence_after();
+      if (leader) {
+        const uint32_t a0 = ring_u + s * TILE_BYTES;
+        const uint32_t b0 = p_u + (i2 & 1) * (NR * TK * 2);
+#pragma unroll
+        for (int ks = 0; ks < TK / 16; ++ks) {
+          const uint64_t a = smem_desc(a0 + ks * 16 * 128, TK * 128, 1024, 2);
+          const uint64_t b = smem_desc(b0 + ks * 2 * 128, 128, TK * 16, 0);
+          umma(tbase + OCOL, a, b, id_pv, (i2 > 0 || ks > 0) ? 1u : 0u);
+        }
+        umma_commit(empty + s);
+        umma_commit(pfree + (i2 & 1));
+        if (i2 == nt - 1) umma_commit(obar);
+      }
+      __syncwarp();
+      ++f;
+    }
+    asm volatile("bar.sync 2, %0;\n" ::"n"((NSW + 1) * 32) : "memory");
+    tc_fence_after();
+    tmem_dealloc(tbase, TCOLS);
+    return;
+  }
+
+  // ===================== softmax warps: thread = (head, key) row of the tile =====================
+  const int row = warp * 32 + lane;
+  const int hh = row / KPT, k = row % KPT;
+  const int hsel = WH > 1 ? (lane / KPT) : 0;            // which of the warp's heads
+  const int col0 = (warp * 32 / KPT) * G;                // first S column the warp reads
+  const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
+  float m[G], l[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) m[g] = -INFINITY, l[g] = 0.f;
+
+  auto load_s = [&](int u, float (&v)[G]) {
+    float w[WH * G];
+    tmem_ld_n<WH * G>(tl + (u % TMAX) * NR + col0, w);
+    tmem_wait_ld();
+#pragma unroll
+    for (int g = 0; g < G; ++g) v[g] = WH > 1 && hsel ? w[G + g] : w[g];
+  };
+  auto key_info = [&](int t, int& pos, float& bias, bool& vis) {
+    const int j = t * KPT + k;
+    pos = spos[j];
+    vis = pos >= 0 && (j < it.crit_len || pos <= it.qpos0);
+    bias = (vis && p.n_planted) ? planted_bias(p.planted, p.n_planted, p.bonus_log2, pos) : 0.f;
+  };
+  auto release = [&](int u) {
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(sfree + u % TMAX);
+  };
+
+  for (int t = 0; t < nt; ++t) {
+    int pos;
+    float bias;
+    bool vis;
+    key_info(t, pos, bias, vis);
+    mbar_wait(sfull + t % TMAX, (t / TMAX) & 1);
+    tc_fence_after();
+    float v[G];
+    load_s(t, v);
+    if (t < nt - TR) release(t);
+    if (vis) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float s2 = fmaf(v[g], p.scale_log2, bias);
+        const float nm = fmaxf(m[g], s2);
+        l[g] = l[g] * ex2(m[g] - nm) + ex2(s2 - nm);
+        m[g] = nm;
+      }
+    }
+  }
+  // statistics of each (head, q head) row: reduce over the KPT lanes of this head
+  float lse[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+#pragma unroll
+    for (int o = KPT / 2; o >= 1; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, m[g], o), ol = __shfl_xor_sync(0xffffffffu, l[g], o);
+      stat_merge(m[g], l[g], om, ol);
+    }
+    lse[g] = m[g] + log2f(l[g]);
+  }
+  if (tid == 0) {
+    HTRACE(2, gtime());
+    HTRACE(3, gtime());
+  }
+
+  const bool scores = p.acc != nullptr && it.acc_row >= 0;
+  for (int i2 = 0; i2 < nt; ++i2) {
+    const int t = i2 < TR ? nt - TR + i2 : i2 - TR;
+    const int u = i2 < TR ? t : nt + t;
+    int pos;
+    float bias;
+    bool vis;
+    key_info(t, pos, bias, vis);
+    mbar_wait(sfull + u % TMAX, (u / TMAX) & 1);
+    tc_fence_after();
+    float v[G];
+    load_s(u, v);
+    release(u);
+    float sum = 0.f;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      v[g] = vis ? ex2(fmaf(v[g], p.scale_log2, bias) - lse[g]) : 0.f;
+      sum += v[g];
+    }
+    if (scores && sum != 0.f) red_add_fx(p.acc + (int64_t)it.acc_row * p.acc_stride + pos, sum, p.acc_scale);
+    if (i2 >= 2) mbar_wait(pfree + (i2 & 1), ((i2 >> 1) - 1) & 1);
+    // P^T row `row`: this head's G columns (the rest of the row stays zero)
+    unsigned char* pb = pbuf + (i2 & 1) * (NR * TK * 2) + row * 16 + ((hh * G) >> 3) * (TK * 16);
+    if constexpr (G == 8) {
+      uint4 w;
+      __nv_bfloat162 b0 = __floats2bfloat162_rn(v[0], v[1]), b1 = __floats2bfloat162_rn(v[2], v[3]);
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(v[4], v[5]), b3 = __floats2bfloat162_rn(v[6], v[7]);
+      w.x = *reinterpret_cast<uint32_t*>(&b0), w.y = *reinterpret_cast<uint32_t*>(&b1);
+      w.z = *reinterpret_cast<uint32_t*>(&b2), w.w = *reinterpret_cast<uint32_t*>(&b3);
+      *reinterpret_cast<uint4*>(pb) = w;
+    } else {
+      static_assert(G == 4, "group size 4 or 8");
+      uint2 w;
+      __nv_bfloat162 b0 = __floats2bfloat162_rn(v[0], v[1]), b1 = __floats2bfloat162_rn(v[2], v[3]);
+      w.x = *reinterpret_cast<uint32_t*>(&b0), w.y = *reinterpret_cast<uint32_t*>(&b1);
+      *reinterpret_cast<uint2*>(pb + ((hh * G) & 7) * 2) = w;
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(pready + (i2 & 1));
+  }
+
+  float o[NR];
+  if (tid == 0) HTRACE(4, gtime());
+  if (nt > 0) {
+    mbar_wait(obar, 0);
+    tc_fence_after();
+    if (tid == 0) HTRACE(5, gtime());
+    tmem_ld_row<NR>(tl + OCOL, o);
+  } else {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) o[r] = 0.f;
+  }
+  tc_fence_before();
+  asm volatile("bar.arrive 2, %0;\n" ::"n"((NSW + 1) * 32) : "memory");
+#pragma unroll
+  for (int r = 0; r < NQ; ++r)
+    p.out[((int64_t)it.q_row0 * p.q_heads + h0 * G + r) * D + row] = __float2bfloat16_rn(o[r]);
+  if (p.lse_out != nullptr && k == 0) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) p.lse_out[(int64_t)it.q_row0 * p.q_heads + (h0 + hh) * G + g] = lse[g] * LN2;
+  }
+  if (tid == 0) HTRACE(6, gtime());
+#undef HTRACE
+}
+
 template <int G, int NR, int NSLOT, int TCOLS>
 __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(const __grid_constant__ Params p) {
   verify_body<G, NR, NSLOT, TCOLS>(p, blockIdx.y, blockIdx.z);
+}
+
+// ---------------------------------------------------------------------------------------
+// f3: one launch for a layer's verify AND draft work.  The grid is the verify launch (C-CTA
+// clusters); a CTA that has finished its verify chunk keeps claiming draft units
+// ((item, group of four kv heads), the head-packed K1 body on the same six warps, one
+// producer) from a launch-tagged global counter until none is left, so the draft work fills
+// the verify launch's tail waves on chip instead of in a second launch.
+struct FusedCtl {
+  unsigned long long* ctr;  // (tag << 32 | next unit), library-owned, never reset
+  uint32_t tag;             // this launch's tag (nonzero)
+  int n_units;              // draft items x (kv heads / 4)
+  int hgroups;              // kv heads / 4
+};
+
+__device__ __forceinline__ int claim_unit(const FusedCtl& fc) {
+  const unsigned long long tagb = (unsigned long long)fc.tag << 32;
+  unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(fc.ctr);
+  while (true) {
+    int got;
+    unsigned long long nv;
+    if ((old & 0xffffffff00000000ull) != tagb) {  // first claim of this launch
+      nv = tagb | 1ull;
+      got = 0;
+    } else {
+      nv = old + 1;
+      got = (int)(old & 0xffffffffull);
+    }
+    const unsigned long long prev = atomicCAS(fc.ctr, old, nv);
+    if (prev == old) return got;
+    old = prev;
+  }
+}
+
+template <int G, int NR, int NSLOT, int TCOLS>
+__global__ void __launch_bounds__(NT, 2) attn_fused_kernel(const __grid_constant__ Params pv,
+                                                           const __grid_constant__ Params pd, const FusedCtl fc) {
+  verify_body<G, NR, NSLOT, TCOLS>(pv, blockIdx.y, blockIdx.z, false);
+  __shared__ int s_unit;
+  __syncthreads();
+  for (;;) {
+    if (threadIdx.x == 0) s_unit = claim_unit(fc);
+    __syncthreads();
+    const int u = s_unit;
+    __syncthreads();
+    if (u >= fc.n_units) break;
+    draft_body<G, 4, 2, 256, 1>(pd, u % fc.hgroups, u / fc.hgroups, false);
+    __syncthreads();
+  }
+}
+
+template <int G, int NR, int NSLOT, int TCOLS>
+int launch_fused(const Params& pv, const Params& pd, const FusedCtl& fc, int C, int num_items, int kv_heads, int smem,
+                 cudaStream_t stream) {
+  auto kern = attn_fused_kernel<G, NR, NSLOT, TCOLS>;
+  static int configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    configured = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, kv_heads, num_items);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, pv, pd, fc);
+  count_launch();
+  if (e != cudaSuccess) {
+    set_error(std::string("sd_attention_pair (fused) launch: ") + cudaGetErrorString(e));
+    return (int)e;
+  }
+  return 0;
 }
 
 // dynamic shared memory / cluster attributes of one instantiation (raised on demand)
@@ -683,6 +1143,11 @@ constexpr int kNarrowMaxNR = 48;
 constexpr int kMaxNR = 80;
 int launch_verify_g4(const Params& prm, int NR, int C, int num_items, int kv_heads, cudaStream_t stream);
 int launch_verify_g8(const Params& prm, int NR, int C, int num_items, int kv_heads, cudaStream_t stream);
+// fused verify + draft launch for the two-CTA-per-SM verify shapes (NR <= 48); -1: no such
+int launch_fused_g4(const Params& pv, const Params& pd, const FusedCtl& fc, int NR, int C, int num_items, int kv_heads,
+                    int smem, cudaStream_t stream);
+int launch_fused_g8(const Params& pv, const Params& pd, const FusedCtl& fc, int NR, int C, int num_items, int kv_heads,
+                    int smem, cudaStream_t stream);
 int verify_slots_g4(int NR, int C, int smem);
 
 int verify_slots_g8(int NR, int C, int smem);

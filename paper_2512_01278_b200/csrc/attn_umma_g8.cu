@@ -21,6 +21,18 @@ int launch_verify_g8(const Params& prm, int NR, int C, int num_items, int kv_hea
   return -1;
 }
 
+int launch_fused_g8(const Params& pv, const Params& pd, const FusedCtl& fc, int NR, int C, int num_items, int kv_heads,
+                    int smem, cudaStream_t stream) {
+  switch (NR) {
+#define X(nr) \
+  case nr: return launch_fused<8, nr, 2, 256>(pv, pd, fc, C, num_items, kv_heads, smem, stream);
+    X(8) X(16) X(24) X(32) X(40) X(48)
+#undef X
+    default: break;
+  }
+  return -1;
+}
+
 int verify_slots_g8(int NR, int C, int smem) {
   switch (NR) {
 #define X(nr, ns, tc) \

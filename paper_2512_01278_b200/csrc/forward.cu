@@ -26,6 +26,9 @@ extern "C" int sd_rmsnorm_cast(const float* x, int32_t rows, int32_t h, float ep
 extern "C" int sd_rope_kv_write(const void* qkv, int64_t qkv_row_stride, int32_t rows, const int32_t* row_table,
                                 const int32_t* row_pos, const sd_paged_kv* kv, int32_t layer, int32_t q_heads,
                                 void* q_out, void* stream);
+extern "C" int sd_attention_pair(const void* q, void* out, const sd_paged_kv* kv, int32_t layer,
+                                 const sd_attn_launch* verify, const sd_attn_launch* draft, const int32_t* planted,
+                                 int32_t num_planted, float planted_bonus, int32_t q_heads, float scale, void* stream);
 extern "C" int sd_attention(const void* q, void* out, float* lse, const sd_paged_kv* kv, int32_t layer,
                             const int32_t* items, int32_t num_items, int32_t max_keys, int32_t max_nq,
                             const int32_t* crit, uint64_t* acc, int64_t acc_row_stride, int32_t acc_shift,
@@ -296,6 +299,10 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
   sd::AttnStreams* as = nullptr;
   const bool overlap = num_launches == 2 && attn_events == nullptr && !(flags & 1) &&
                        launches[0].num_items > 0 && launches[1].num_items > 0 && (as = sd::attn_streams()) != nullptr;
+  // f3 fused verify + draft launch (flags bit 1): launch 0 dense verify, launch 1 drafts
+  const bool fused = (flags & 2) && num_launches == 2 && attn_events == nullptr && launches[0].num_items > 0 &&
+                     launches[1].num_items > 0 && launches[0].crit == nullptr && launches[1].crit != nullptr &&
+                     launches[1].max_nq == 1;
   int rc;
   for (int l = 0; l < layers; ++l) {
     if ((rc = sd_rmsnorm_cast(x, rows, hidden, eps, hn, SD_DTYPE_BF16, stream)) != 0) return rc;
@@ -304,6 +311,13 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
       sd::rope_kv_write_table(qkv, qkv_w, rows, row_table, row_pos, kv, l, q_heads, table, q, s);
     else if ((rc = sd_rope_kv_write(qkv, qkv_w, rows, row_table, row_pos, kv, l, q_heads, q, stream)) != 0)
       return rc;
+    if (fused) {
+      // f3: one launch, the verify grid's CTAs take the draft units after their verify chunk
+      rc = sd_attention_pair(q, ctx, kv, l, &launches[0], &launches[1], planted, num_planted, planted_bonus, q_heads,
+                             scale, stream);
+      if (rc == 0) goto attn_done;
+      if (rc != 1) return rc;
+    }
     if (overlap) {
       // K2 (launch 0) high priority, K1 (launch 1) low priority, concurrently
       cudaEventRecord(as->fork, s);
@@ -331,6 +345,7 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
         if (ev && ev[1]) cudaEventRecord(ev[1], s);
       }
     }
+  attn_done:
     if ((rc = sd::gemm(hd, rows, hidden, hidden, ctx, w[l].wo, x, true, 1.f)) != 0) return rc;
     if ((rc = sd_rmsnorm_cast(x, rows, hidden, eps, hn, SD_DTYPE_BF16, stream)) != 0) return rc;
     if ((rc = sd::gemm(hd, rows, 2 * hidden, hidden, hn, w[l].mlp_in, hm, false, 0.f)) != 0) return rc;

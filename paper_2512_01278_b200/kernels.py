@@ -91,6 +91,30 @@ def attention(q: torch.Tensor, out: torch.Tensor, pool, layer: int, items: torch
             "sd_attention")
 
 
+def attention_pair(q: torch.Tensor, out: torch.Tensor, pool, layer: int, verify: dict, draft: dict, q_heads: int,
+                   *, planted: torch.Tensor | None = None, planted_bonus: float = 0.0,
+                   scale: float | None = None) -> bool:
+    """f3: a layer's verify launch (dense items; keys items / num_items / max_keys / max_nq /
+    acc / acc_row_stride / acc_shift) and draft launch (items / num_items / max_keys / crit) in
+    ONE launch.  Returns False (nothing launched) when the pair does not qualify."""
+    def desc(d):
+        return N.AttnLaunchDesc(d["items"].data_ptr(), d["num_items"], d["max_keys"], d.get("max_nq", 1),
+                                d.get("acc_shift", 0), N.ptr(d.get("crit")), N.ptr(d.get("acc")),
+                                d.get("acc_row_stride", 0))
+    dv, dd = desc(verify), desc(draft)
+    if scale is None:
+        scale = 1.0 / (pool.head_dim ** 0.5)
+    n_planted = 0 if planted is None else planted.numel()
+    pdesc = pool.desc()
+    rc = N.lib().sd_attention_pair(q.data_ptr(), out.data_ptr(), ctypes.byref(pdesc), layer, ctypes.byref(dv),
+                                   ctypes.byref(dd), N.ptr(planted), n_planted, planted_bonus, q_heads, scale,
+                                   N.stream_handle())
+    if rc == 1:
+        return False
+    N.check(rc, "sd_attention_pair")
+    return True
+
+
 def select_critical(acc: torch.Tensor, acc_req_stride: int, acc_row_stride: int, acc_shift: int,
                     n_rows: torch.Tensor, kv_len: torch.Tensor, sparsity: float, num: int,
                     importance: torch.Tensor, crit: torch.Tensor, crit_len: torch.Tensor,

@@ -598,3 +598,48 @@ def test_linear_tuned_cublaslt_matches_fp32(R, N, Kd):
     assert (out - ref).abs().max().item() <= 1e-3 * scale + 1e-4
     assert (x - (x0 + ref)).abs().max().item() <= 1e-3 * scale + 1e-4
     assert (ob.float() - ref).abs().max().item() <= 1e-2 * scale + 1e-3
+
+
+@pytest.mark.parametrize("G", [4, 8])
+def test_fused_verify_draft_launch_matches_separate_launches(G):
+    """f3: verify items (dense, score emission) and draft items (critical list + fresh tail) in
+    ONE launch (sd_attention_pair) give bitwise the outputs and fixed-point scores of the two
+    separate launches (same tcgen05 bodies), and the separate launches match the oracle
+    (tests above)."""
+    rng = np.random.default_rng(50 + G)
+    Hkv, d, nq = 8, 128, 5
+    Hq = Hkv * G
+    lens_v = [4000, 1200, 2600]
+    lens_d = [3000, 800, 5000, 1700, 2200]
+    B = len(lens_v) + len(lens_d)
+    maxn = max(lens_v + lens_d) + nq
+    pool = _pool(1, Hkv, d, maxn, B, torch.bfloat16, shuffle_seed=7)
+    for r, n in enumerate(lens_v + lens_d):
+        _fill(pool, r, n + nq, rng, scale=0.5)
+    nv = len(lens_v)
+    v_items = make_items([(r, r * nq, nq, n, 0, 0, 0, r * nq, 1) for r, n in enumerate(lens_v)], DEV)
+    bud = [max(1, n // (20 if G == 4 else 40)) for n in lens_d]  # critical lists stay TMEM-resident
+    crit = np.zeros((len(lens_d), max(bud)), dtype=np.int32)
+    for i, n in enumerate(lens_d):
+        crit[i, :bud[i]] = np.sort(rng.choice(n, bud[i], replace=False))
+    crit_d = torch.from_numpy(crit.reshape(-1)).to(DEV)
+    j = 2  # third draft of the round: fresh tail n .. n + 2
+    d_rows = [(nv + i, nv * nq + i, 1, n + j, i * crit.shape[1], bud[i], n, -1, 0) for i, n in enumerate(lens_d)]
+    d_items = make_items(d_rows, DEV)
+    R = nv * nq + len(lens_d)
+    q = torch.from_numpy(rng.normal(size=(R, Hq, d))).to(DEV, torch.bfloat16)
+    runs = []
+    for fused in (False, True):
+        out = torch.zeros(R, Hq, d, dtype=torch.bfloat16, device=DEV)
+        acc, shift = _acc(nv * nq, maxn, Hq)
+        v = dict(items=v_items, num_items=nv, max_keys=maxn, max_nq=nq, acc=acc, acc_row_stride=maxn, acc_shift=shift)
+        dr = dict(items=d_items, num_items=len(lens_d), max_keys=max(bud) + j + 1, crit=crit_d)
+        if fused:
+            assert K.attention_pair(q, out, pool, 0, v, dr, Hq)
+        else:
+            K.attention(q, out, pool, 0, v_items, nv, maxn, nq, Hq, acc=acc, acc_row_stride=maxn, acc_shift=shift)
+            K.attention(q, out, pool, 0, d_items, len(lens_d), max(bud) + j + 1, 1, Hq, crit=crit_d)
+        torch.cuda.synchronize()
+        runs.append((out.clone(), acc.clone()))
+    assert torch.equal(runs[0][0], runs[1][0])
+    assert torch.equal(runs[0][1], runs[1][1])

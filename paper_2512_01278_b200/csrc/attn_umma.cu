@@ -285,19 +285,20 @@ int launch_attn_pair(const void* q, void* out, const sd_paged_kv* kvp, int layer
   const int smem = std::max(make_layout(pl.NR, 2, Sv, pl.chunk / TK, 1).total, make_hp_layout(NRd, 2, tmax, ct).total);
   if (smem > 113 * 1024) return 1;
   static std::mutex mu;
-  static unsigned long long* ctr[64] = {};
-  static std::atomic<uint32_t> tag{0};
+  static unsigned int* ctr[64] = {};
+  static int parity[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
+  int par;
   {
     std::lock_guard<std::mutex> lock(mu);
     if (ctr[dev & 63] == nullptr) {
-      if (cudaMalloc(&ctr[dev & 63], sizeof(unsigned long long)) != cudaSuccess) return 1;
-      cudaMemset(ctr[dev & 63], 0, sizeof(unsigned long long));
+      if (cudaMalloc(&ctr[dev & 63], 4 * sizeof(unsigned int)) != cudaSuccess) return 1;
+      cudaMemset(ctr[dev & 63], 0, 4 * sizeof(unsigned int));
     }
+    par = parity[dev & 63];
+    parity[dev & 63] ^= 1;
   }
-  uint32_t tg = tag.fetch_add(1) + 1;
-  if (tg == 0) tg = tag.fetch_add(1) + 1;
   Params pv{}, pd{};
   pv.q = pd.q = static_cast<const __nv_bfloat16*>(q);
   pv.out = pd.out = static_cast<__nv_bfloat16*>(out);
@@ -323,7 +324,9 @@ int launch_attn_pair(const void* q, void* out, const sd_paged_kv* kvp, int layer
   pd.items = d_items;
   pd.crit = d_crit;
   pd.chunk = ct * TK;
-  FusedCtl fc{ctr[dev & 63], tg, d_n * (kvp->kv_heads / 4), kvp->kv_heads / 4};
+  static const int any_cta = env_int("SD_FUSED_ANY", 0);
+  FusedCtl fc{ctr[dev & 63], par, d_n * (kvp->kv_heads / 4), kvp->kv_heads / 4, pl.C * kvp->kv_heads * v_n, any_cta};
+  if (env_int("SD_FUSED_NODRAFT", 0)) fc.n_units = 0;  // diagnostics: the verify part alone
   const int rc = G == 4 ? launch_fused_g4(pv, pd, fc, pl.NR, pl.C, v_n, kvp->kv_heads, smem, stream)
                         : launch_fused_g8(pv, pd, fc, pl.NR, pl.C, v_n, kvp->kv_heads, smem, stream);
   return rc < 0 ? 1 : rc;

@@ -44,6 +44,8 @@
 namespace sd {
 namespace umma_attn {
 
+constexpr uint32_t kNoTmem = 0xffffffffu;
+
 // TMEM columns loaded per step by the softmax warps (bounds live registers at large NR)
 template <int NR>
 constexpr int col_chunk() {
@@ -108,7 +110,8 @@ __device__ __forceinline__ void rows_reduce_store(float* m, float* l, int lane, 
 }
 
 template <int G, int NR, int NSLOT, int TCOLS>
-__device__ __forceinline__ void verify_body(const Params& p, const int h, const int item_idx, bool relinquish = true) {
+// ext_tmem: a TMEM base the caller allocated (the fused kernel), or kNoTmem to allocate here
+__device__ __forceinline__ void verify_body(const Params& p, const int h, const int item_idx, uint32_t ext_tmem = kNoTmem) {
   constexpr int S = TCOLS / NR;             // logits slots (slot S-1 = O^T accumulator)
   constexpr int OCOL = (S - 1) * NR;
   constexpr int CH = col_chunk<NR>();
@@ -166,7 +169,7 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
   const bool use_tma = p.tma && p.dense && ((it.dense_lo + kb) & 15) == 0;
 
   // ---- setup ----
-  if (warp == WMMA) tmem_alloc(tptr, TCOLS, relinquish);
+  if (warp == WMMA && ext_tmem == kNoTmem) tmem_alloc(tptr, TCOLS);
   if (tid == 0) {
     // TMA fills: one arrival with the transaction bytes; cp.async fills: one per producer lane
     for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, use_tma ? 1 : 32), mbar_init(empty + i, 1);
@@ -218,7 +221,7 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = *tptr;
+  const uint32_t tbase = ext_tmem == kNoTmem ? *tptr : ext_tmem;
   if (warp < NSW) {
     // Q rows (token-major: r = tok*G + g) -> [dhalf][NR][128 B] SWIZZLE_128B, zero padding rows
     for (int i = tid; i < NR * 16; i += NSW * 32) {
@@ -385,7 +388,7 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
     }
     asm volatile("bar.sync 2, %0;\n" ::"n"((NSW + 1) * 32) : "memory");  // softmax warps read O
     tc_fence_after();
-    tmem_dealloc(tbase, TCOLS);
+    if (ext_tmem == kNoTmem) tmem_dealloc(tbase, TCOLS);
     return;
   }
 
@@ -672,7 +675,7 @@ constexpr int HP_NPROD = 4;
 constexpr int HP_NT = (NSW + HP_NPROD + 1) * 32;
 
 template <int G, int HPC, int NSLOT, int TCOLS, int NPROD = HP_NPROD>
-__device__ __forceinline__ void draft_body(const Params& p, const int hgroup, const int item_idx, bool relinquish = true) {
+__device__ __forceinline__ void draft_body(const Params& p, const int hgroup, const int item_idx, uint32_t ext_tmem = kNoTmem) {
   constexpr int HP_WPROD = NSW, HP_WMMA = NSW + NPROD;
   constexpr int BNT = (NSW + NPROD + 1) * 32;
   constexpr int NQ = HPC * G;                       // q heads of the CTA
@@ -719,7 +722,7 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
   uint64_t* obar = pfree + 2;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L.tptr);
 
-  if (warp == HP_WMMA) tmem_alloc(tptr, TCOLS, relinquish);
+  if (warp == HP_WMMA && ext_tmem == kNoTmem) tmem_alloc(tptr, TCOLS);
   if (tid == 0) {
     for (int i = 0; i < NSLOT; ++i) mbar_init(full + i, 32 * NPROD), mbar_init(empty + i, 1);
     for (int i = 0; i < TMAX; ++i) mbar_init(sfull + i, 1), mbar_init(sfree + i, NSW);
@@ -761,7 +764,7 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = *tptr;
+  const uint32_t tbase = ext_tmem == kNoTmem ? *tptr : ext_tmem;
   if (tid == 0) HTRACE(1, gtime());
 
   const int64_t row_stride = (int64_t)p.kv.kv_heads * D;
@@ -850,7 +853,7 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
     }
     asm volatile("bar.sync 2, %0;\n" ::"n"((NSW + 1) * 32) : "memory");
     tc_fence_after();
-    tmem_dealloc(tbase, TCOLS);
+    if (ext_tmem == kNoTmem) tmem_dealloc(tbase, TCOLS);
     return;
   }
 
@@ -997,45 +1000,60 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
 // producer) from a launch-tagged global counter until none is left, so the draft work fills
 // the verify launch's tail waves on chip instead of in a second launch.
 struct FusedCtl {
-  unsigned long long* ctr;  // (tag << 32 | next unit), library-owned, never reset
-  uint32_t tag;             // this launch's tag (nonzero)
-  int n_units;              // draft items x (kv heads / 4)
-  int hgroups;              // kv heads / 4
+  unsigned int* ctr;  // [2 launch parities][next draft unit, verify CTAs started]: zero at the
+                      // start of a launch (launch t clears parity t + 1 for the next launch on
+                      // the stream), so plain atomicAdd, no reset launch
+  int parity;         // this launch's counter pair
+  int n_units;        // draft items x (kv heads / 4)
+  int hgroups;        // kv heads / 4
+  int n_ctas;         // verify CTAs of the launch
+  int any_cta;        // 1: every CTA takes draft units after its verify chunk; 0: only those
+                      // finishing once every verify CTA has started (the last wave)
 };
-
-__device__ __forceinline__ int claim_unit(const FusedCtl& fc) {
-  const unsigned long long tagb = (unsigned long long)fc.tag << 32;
-  unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(fc.ctr);
-  while (true) {
-    int got;
-    unsigned long long nv;
-    if ((old & 0xffffffff00000000ull) != tagb) {  // first claim of this launch
-      nv = tagb | 1ull;
-      got = 0;
-    } else {
-      nv = old + 1;
-      got = (int)(old & 0xffffffffull);
-    }
-    const unsigned long long prev = atomicCAS(fc.ctr, old, nv);
-    if (prev == old) return got;
-    old = prev;
-  }
-}
 
 template <int G, int NR, int NSLOT, int TCOLS>
 __global__ void __launch_bounds__(NT, 2) attn_fused_kernel(const __grid_constant__ Params pv,
                                                            const __grid_constant__ Params pd, const FusedCtl fc) {
-  verify_body<G, NR, NSLOT, TCOLS>(pv, blockIdx.y, blockIdx.z, false);
+  // one TMEM allocation (256 columns) for both bodies
+  __shared__ uint32_t s_tmem;
   __shared__ int s_unit;
+  unsigned int* my = fc.ctr + 2 * fc.parity;
+  if ((threadIdx.x >> 5) == WMMA) tmem_alloc(&s_tmem, TCOLS);
+  if (threadIdx.x == 0) {
+    atomicAdd(my + 1, 1u);  // this verify CTA has started
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {  // the next launch's pair
+      fc.ctr[2 * (fc.parity ^ 1)] = 0;
+      fc.ctr[2 * (fc.parity ^ 1) + 1] = 0;
+    }
+  }
+  tc_fence_before();
   __syncthreads();
-  for (;;) {
-    if (threadIdx.x == 0) s_unit = claim_unit(fc);
+  tc_fence_after();
+  const uint32_t tm = s_tmem;
+  verify_body<G, NR, NSLOT, TCOLS>(pv, blockIdx.y, blockIdx.z, tm);
+  // only CTAs finishing once every verify CTA has started take draft units: earlier ones
+  // leave their cluster's slots to the verify clusters still waiting (no fragmentation),
+  // the last wave's CTAs fill its tail with the drafts
+  if (threadIdx.x == 0)
+    s_unit = fc.any_cta || *reinterpret_cast<volatile unsigned int*>(my + 1) >= (unsigned)fc.n_ctas ? 0 : -1;
+  __syncthreads();
+  if (s_unit >= 0) {
     __syncthreads();
-    const int u = s_unit;
-    __syncthreads();
-    if (u >= fc.n_units) break;
-    draft_body<G, 4, 2, 256, 1>(pd, u % fc.hgroups, u / fc.hgroups, false);
-    __syncthreads();
+    for (;;) {
+      if (threadIdx.x == 0) s_unit = (int)atomicAdd(my, 1u);
+      __syncthreads();
+      const int u = s_unit;
+      __syncthreads();
+      if (u >= fc.n_units) break;
+      draft_body<G, 4, 2, 256, 1>(pd, u % fc.hgroups, u / fc.hgroups, tm);
+      __syncthreads();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if ((threadIdx.x >> 5) == WMMA) {
+    tc_fence_after();
+    tmem_dealloc(tm, TCOLS);
   }
 }
 

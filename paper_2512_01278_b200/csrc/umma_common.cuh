@@ -77,11 +77,9 @@ __device__ __forceinline__ void red_add_fx(unsigned long long* p, float v, float
 }
 
 // ---- tensor memory / UMMA ----
-// relinquish = false keeps the CTA's permit to allocate again (the fused verify + draft
-// kernel allocates once per body)
-__device__ __forceinline__ void tmem_alloc(uint32_t* dst, int cols, bool relinquish = true) {
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, int cols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst)), "r"(cols));
-  if (relinquish) asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
 }
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, int cols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(cols));

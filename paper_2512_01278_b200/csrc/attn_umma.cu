@@ -326,7 +326,6 @@ int launch_attn_pair(const void* q, void* out, const sd_paged_kv* kvp, int layer
   pd.chunk = ct * TK;
   static const int any_cta = env_int("SD_FUSED_ANY", 0);
   FusedCtl fc{ctr[dev & 63], par, d_n * (kvp->kv_heads / 4), kvp->kv_heads / 4, pl.C * kvp->kv_heads * v_n, any_cta};
-  if (env_int("SD_FUSED_NODRAFT", 0)) fc.n_units = 0;  // diagnostics: the verify part alone
   const int rc = G == 4 ? launch_fused_g4(pv, pd, fc, pl.NR, pl.C, v_n, kvp->kv_heads, smem, stream)
                         : launch_fused_g8(pv, pd, fc, pl.NR, pl.C, v_n, kvp->kv_heads, smem, stream);
   return rc < 0 ? 1 : rc;

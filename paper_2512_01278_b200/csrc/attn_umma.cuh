@@ -995,10 +995,12 @@ __global__ void __launch_bounds__(NT, TCOLS == 512 ? 1 : 2) attn_umma_kernel(con
 
 // ---------------------------------------------------------------------------------------
 // f3: one launch for a layer's verify AND draft work.  The grid is the verify launch (C-CTA
-// clusters); a CTA that has finished its verify chunk keeps claiming draft units
-// ((item, group of four kv heads), the head-packed K1 body on the same six warps, one
-// producer) from a launch-tagged global counter until none is left, so the draft work fills
-// the verify launch's tail waves on chip instead of in a second launch.
+// clusters); a CTA that has finished its verify chunk (only once every verify CTA has
+// started, unless any_cta) keeps claiming draft units ((item, group of four kv heads), the
+// head-packed K1 body on the same six warps, one producer) from a global counter until none
+// is left, so the draft work fills the verify launch's tail waves on chip instead of in a
+// second launch.  Measured against the two launches on priority streams it loses (DESIGN.md
+// §0 f3), so the layer loop uses it only with SD_ATTN_FUSED=1.
 struct FusedCtl {
   unsigned int* ctr;  // [2 launch parities][next draft unit, verify CTAs started]: zero at the
                       // start of a launch (launch t clears parity t + 1 for the next launch on

@@ -177,7 +177,6 @@ struct Params {
   float scale_log2;
   int chunk;  // keys per CTA, multiple of TK
   int dense;  // 1: items have no critical list and pages >= 16 tokens (page ids staged, not slots)
-  int dbg;    // diagnostics (SD_ATTN_DBG): timing experiments only
 };
 
 // (m, l) softmax-statistics merge

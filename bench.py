@@ -513,12 +513,18 @@ def main():
     import torch
     import torch.distributed as dist
 
+    if os.environ.get("SD_BENCH_SHARE_GPU"):
+        # diagnostics: several ranks on one GPU (multi-rank code path test on a 1-GPU box; gloo)
+        local_rank = local_rank % torch.cuda.device_count()
     if world > 1:
         # NCCL INFO on stderr: the communicator's nranks / transport are checkable from the log
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("SD_BENCH_SHARE_GPU"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_ours(args, rank, world, local_rank)
     if rank == 0:
         m = res["main"]

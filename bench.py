@@ -11,13 +11,15 @@ A "step" is one unified draft/verify iteration over the whole batch
 ((k+1)-row K2 items with score emission) and the rest draft members (K1
 items over their critical sets), one batched forward, K4 accept, K3 refresh.
 
-The timed window sits at the run's MID-POINT context (prompt 512 + 4096
-already-generated tokens = 4608 KV rows per request): per-iteration cost is
-linear in context, so this equals the mean over the full 8K-output run.  Setup
-(untimed): the 512-token prompt and 4096 teacher-forced continuation tokens are
-prefilled through the same kernels (scores captured -> first critical set; ~10 s
-for 128 requests; --synthetic-prefill writes the continuation's K/V directly
-instead).  KV capacity for the full 8K run is allocated up front.
+The K timed iterations are split over FOUR windows at the contexts where 1/8, 3/8,
+5/8 and 7/8 of the 8K output are generated (1536 / 3584 / 5632 / 7680 KV rows per
+request): tokens / time over them is the midpoint-rule estimate of the whole run's
+throughput (per-iteration cost grows with context, not quite linearly: measured
+7.05 / 8.36 / 12.38 ms at contexts 2560 / 4608 / 8640).  Setup of each window
+(untimed): the 512-token prompt and the teacher-forced continuation up to the
+window's context are prefilled through the same kernels (scores captured -> first
+critical set; --synthetic-prefill writes the continuation's K/V directly instead).
+KV capacity for the full 8K run is allocated up front.
 
 Setup (untimed): prefill, then an 8-iteration pre-roll (first-round phase stagger,
 cuBLAS shape caches), then W warm-up iterations.  The K timed iterations contain
@@ -66,13 +68,14 @@ def parse():
                         "512 = configs[2] at >1 GPU); a rank runs its shard in waves of --batch")
     p.add_argument("--prompt", type=int, default=512)
     p.add_argument("--output", type=int, default=8192)
-    p.add_argument("--context", type=int, default=None, help="KV rows at the timed window (default prompt+output/2)")
+    p.add_argument("--context", type=int, default=None,
+                   help="time ONE window at this many KV rows instead of the four run-quantile windows")
     p.add_argument("--k", type=int, default=4)
     p.add_argument("--sparsity", type=float, default=0.05)
     p.add_argument("--layers", type=int, default=C1["layers"])
     p.add_argument("--variants", default="planted,sweep,c3",
-                   help="comma list of extra variants: planted (alpha ~ 1), sweep (s = 1/2/10%%), c3 (configs[3] "
-                        "32B-shaped), none")
+                   help="comma list of extra variants: planted (alpha ~ 1), sweep (s = 1/2/10%%), ctx (early / late "
+                        "timed windows), c3 (configs[3] 32B-shaped), none")
     p.add_argument("--pool", choices=["full", "window"], default="full")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--synthetic-prefill", action="store_true",
@@ -220,7 +223,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         prev, dec._bench_pending = getattr(dec, "_bench_pending", None), None
         return dec.complete(prev) if prev is not None else None
 
-    def measure(m, steps, warmup, label, with_roofline, **dims):
+    def measure(m, steps, warmup, label, with_roofline, clocks=None, **dims):
         """Warm up, then time `steps` iterations with NOTHING but the iterations in the
         timed region (no per-launch events); afterwards, if asked, run a few more
         iterations with per-launch CUDA events on the K1 / K2 launches for the roofline."""
@@ -235,7 +238,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        sampler = (ClockSampler(local_rank) if (rank == 0 and with_roofline and not os.environ.get("SD_BENCH_NO_CLOCKS"))
+        want_clocks = with_roofline if clocks is None else clocks
+        sampler = (ClockSampler(local_rank) if (rank == 0 and want_clocks and not os.environ.get("SD_BENCH_NO_CLOCKS"))
                    else None)
         if sampler:
             sampler.start()
@@ -325,22 +329,43 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     n_waves = torch.tensor([len(waves)], device=dev)
     if world > 1:
         dist.all_reduce(n_waves, op=dist.ReduceOp.MAX)
+    # the run's throughput: K timed iterations split over windows at the contexts where 1/8,
+    # 3/8, 5/8, 7/8 of the output are generated (midpoint rule); the K1 / K2 roofline pass runs
+    # in every window of the first wave (bytes and launch times summed: the run's average), the
+    # clock sampler and the NVTX "timed_random" range in the window nearest the mid-run context
+    if args.context:
+        windows = [args.context]
+    else:
+        windows = [args.prompt + (2 * i + 1) * args.output // 8 for i in range(4)]
+    roof_w = min(range(len(windows)), key=lambda i: abs(windows[i] - (args.prompt + args.output // 2)))
+    wsteps = [args.steps // len(windows) + (1 if i < args.steps % len(windows) else 0) for i in range(len(windows))]
     main = None
     for wi in range(int(n_waves.item())):
         ids = waves[wi] if wi < len(waves) else []
-        if not ids:  # a rank with fewer waves still joins the barriers
-            if world > 1:
-                dist.barrier()
-                dist.barrier()
-            continue
-        r = measure(model, args.steps, args.warmup, "random" if wi == 0 else f"random_w{wi}", wi == 0,
-                    B=len(ids), ids=ids)
-        if main is None:
-            main = r
-        else:
-            for key in ("emitted", "dev_s", "wall_s"):
-                main[key] += r[key]
-        log(f"wave {wi} ({len(ids)} requests) done")
+        for ci, cw in enumerate(windows):
+            if wsteps[ci] == 0:
+                continue
+            if not ids:  # a rank with fewer waves still joins the barriers
+                if world > 1:
+                    dist.barrier()
+                    dist.barrier()
+                continue
+            first = wi == 0 and ci == roof_w
+            r = measure(model, wsteps[ci], args.warmup, "random" if first else f"random_w{wi}_c{cw}", wi == 0,
+                        clocks=first, B=len(ids), ids=ids, ctx=cw)
+            if main is None:
+                main = {"emitted": 0, "dev_s": 0.0, "wall_s": 0.0}
+            summed = ("emitted", "dev_s", "wall_s", "verify_launches", "verify_ms_total", "verify_bytes",
+                      "draft_launches", "draft_ms_total", "draft_bytes")
+            for key in summed:
+                if key in r:
+                    main[key] = main.get(key, 0) + r[key]
+            if first:
+                for key, v in r.items():
+                    if key not in summed:
+                        main[key] = v
+            log(f"wave {wi} ({len(ids)} requests), context {cw}: {r['emitted'] / r['dev_s']:.0f} tok/s")
+    main["windows"] = windows
     main["waves"] = len(waves)
     main["per_rank"] = len(my_ids)
     main["global_batch"] = G_total
@@ -360,6 +385,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
             variants[f"budget_s{sv:g}"] = measure(model, max(3, args.steps // 4), 3, f"s{sv:g}", False)
             log(f"budget s={sv:g} done")
         s = base_s
+    if "ctx" in extra:
+        # the timed window sits at the run's mid-point context because per-iteration cost is
+        # linear in context; these two windows (early / late in the 8K-output run) show it
+        for cv in (args.prompt + args.output // 4, args.prompt + args.output - 64):
+            variants[f"context_{cv}"] = measure(model, max(3, args.steps // 4), 3, f"ctx{cv}", False, ctx=cv)
+            variants[f"context_{cv}"]["context"] = cv
+            log(f"context {cv} done")
     if "c3" in extra:
         # configs[3]: Qwen3-32B-shaped (oracle family: h = 64 x 128, GQA 8) long-reasoning decode,
         # 32K output, batch 64 on ONE GPU with the paged KV near HBM capacity: the pool gets
@@ -387,7 +419,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     total_emitted, dev_s = gather_throughput(main["emitted"], main["dev_s"], device=dev)
     _, wall_s = gather_throughput(0.0, main["wall_s"], device=dev)
     results = {"main": main, "variants": variants, "total_emitted": total_emitted, "dev_s": dev_s,
-               "wall_s": wall_s, "ctx": ctx}
+               "wall_s": wall_s, "ctx": ctx, "windows": main["windows"]}
     for name, v in variants.items():
         vv = torch.tensor([v["emitted"], v["dev_s"]], dtype=torch.float64, device=dev)
         if world > 1:
@@ -557,6 +589,9 @@ def main():
         variants = {}
         for name, v in res["variants"].items():
             variants[name] = {"value": v["total_emitted"] / v["dev_s_max"], "unit": "tokens/s", "alpha": v["alpha"]}
+            if v.get("context"):
+                variants[name]["context"] = v["context"]
+                variants[name]["ms_per_step"] = v["dev_s_max"] / max(3, args.steps // 4) * 1000.0
             if v.get("workload"):
                 variants[name]["workload"] = v["workload"]
                 variants[name]["ms_per_step"] = v["dev_s_max"] / max(3, args.steps // 2) * 1000.0
@@ -572,18 +607,21 @@ def main():
                         f"bf16, global batch {job} request-sharded over {args.gpus} GPUs ({m['per_rank']} per rank, "
                         f"waves of <= {args.batch} resident: {m['waves']} on rank 0), prompt {args.prompt}, output "
                         f"{args.output}, k={args.k}, s={args.sparsity}; each wave timed over {args.steps} iterations "
-                        f"at mid-run context {res['ctx']}")
+                        f"split over contexts {'/'.join(str(c) for c in res['windows'])} (1/8, 3/8, 5/8, 7/8 of the "
+                        f"run)")
         else:
             workload = (f"configs[1]: Qwen3-8B-shaped (L={args.layers}, Hq=32, Hkv=8, d=128, V=151936) random-init "
                         f"bf16, batch {job}/GPU, prompt {args.prompt}, output {args.output}, k={args.k}, "
-                        f"s={args.sparsity}; timed window at mid-run context {res['ctx']}")
+                        f"s={args.sparsity}; {args.steps} timed iterations split over contexts "
+                        f"{'/'.join(str(c) for c in res['windows'])} (1/8, 3/8, 5/8, 7/8 of the run: midpoint-rule "
+                        f"estimate of the whole run); K1 / K2 roofline over all four windows")
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": res["dev_s"] / (args.steps * m["waves"]) * 1000.0,
+            "warmup": args.warmup, "ms_per_step": res["dev_s"] / (max(1, args.steps) * m["waves"]) * 1000.0,
             "higher_is_better": True,
             "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (random-init weights, synthetic prompts + teacher-forced continuation to the mid-run "
-                    "context)",
+            "data": "synthetic (random-init weights, synthetic prompts + teacher-forced continuation to each "
+                    "window's context)",
             "config": {"workload": workload, "global_batch": job,
                        "parallelism": f"dp{args.gpus} (request shards, no hot-path collective)",
                        "l2": "inputs larger than L2 (~30 GB read per step)", "pipeline": "delayed (iteration i's verify outcomes are applied on the host during "

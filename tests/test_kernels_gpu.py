@@ -436,17 +436,18 @@ def test_rope_kv_write_matches_oracle():
         assert np.array_equal(vv[0, 1].double().cpu().numpy(), want_v.astype(np.float32).astype(np.float64))
 
 
-def _verify_case(n0s, nq, G, Hkv=8, seed=0, shuffle=5, scale=1.0, planted=()):
+def _verify_case(n0s, nq, G, Hkv=8, seed=0, shuffle=5, scale=1.0, planted=(), page=16, lo=0):
     """One launch of len(n0s) verify items (nq tokens each) vs the oracle: outputs, lse and
-    per-token fixed-point scores (model.py:229-253, selection.py:78-135)."""
+    per-token fixed-point scores (model.py:229-253, selection.py:78-135).  ``lo``: the
+    items' dense range starts there (a window; lo % 16 != 0 takes the cp.async producer)."""
     rng = np.random.default_rng(seed)
     d, Hq = 128, Hkv * G
     B = len(n0s)
     maxn = max(n0s) + nq
-    pool = _pool(1, Hkv, d, maxn, B, torch.bfloat16, shuffle_seed=shuffle)
+    pool = _pool(1, Hkv, d, maxn, B, torch.bfloat16, page=page, shuffle_seed=shuffle)
     for r, n in enumerate(n0s):
         _fill(pool, r, n + nq, rng, scale=scale)
-    items = make_items([(r, r * nq, nq, n, 0, 0, 0, r * nq, 1) for r, n in enumerate(n0s)], DEV)
+    items = make_items([(r, r * nq, nq, n, 0, 0, lo, r * nq, 1) for r, n in enumerate(n0s)], DEV)
     q = torch.from_numpy(rng.normal(size=(B * nq, Hq, d))).to(DEV, torch.bfloat16)
     out = torch.empty_like(q)
     lse = torch.empty(B * nq, Hq, dtype=torch.float32, device=DEV)
@@ -459,7 +460,7 @@ def _verify_case(n0s, nq, G, Hkv=8, seed=0, shuffle=5, scale=1.0, planted=()):
         kr, vr = pool.read(r, range(n + nq))
         kr, vr = kr.double().cpu().numpy()[:, 0], vr.double().cpu().numpy()[:, 0]
         sl = slice(r * nq, (r + 1) * nq)
-        ro, rl, ra = _ref_rows(q[sl].double().cpu().numpy(), kr, vr, Hq, Hkv, d, [], range(n + nq), n,
+        ro, rl, ra = _ref_rows(q[sl].double().cpu().numpy(), kr, vr, Hq, Hkv, d, [], range(lo, n + nq), n,
                                planted=planted, bonus=1.5)
         assert np.abs(out[sl].double().cpu().numpy() - ro).max() <= 2e-2, (r, n)
         assert np.abs(lse[sl].double().cpu().numpy() - rl).max() <= 2e-2, (r, n)
@@ -643,3 +644,10 @@ def test_fused_verify_draft_launch_matches_separate_launches(G):
         runs.append((out.clone(), acc.clone()))
     assert torch.equal(runs[0][0], runs[1][0])
     assert torch.equal(runs[0][1], runs[1][1])
+
+
+@pytest.mark.parametrize("page,lo", [(32, 0), (64, 0), (16, 37), (16, 512)])
+def test_verify_page_sizes_and_windows_bf16(page, lo):
+    """K2 producer paths: TMA 16-key boxes inside 32 / 64-token pages, a window starting off a
+    16-key boundary (cp.async rows) and on one (TMA)."""
+    _verify_case([3000, 1100, 4500], 5, 4, seed=page + lo, page=page, lo=lo)

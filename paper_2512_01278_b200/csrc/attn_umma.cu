@@ -227,24 +227,36 @@ int launch_attn_umma(const void* q, void* out, float* lse, const sd_paged_kv* kv
     prm.trace = g_trace_buf;
   }
   static const int hp_env = env_int("SD_UMMA_HP", 1);
-  if (hp_env && max_nq == 1 && kvp->dtype == SD_DTYPE_BF16 && kvp->head_dim == D && (G == 4 || G == 8) &&
-      kvp->kv_heads % 4 == 0) {
-    // K1: 4 heads per CTA, 32 keys per tile, the whole key list in one CTA
-    const int NR = 4 * G, tmax = (256 - NR) / NR;
-    const int ct_tiles = (max(max_keys, 1) + 31) / 32;      // 32-key tiles
-    const int ct = (ct_tiles * 32 + TK - 1) / TK;           // 128-key units for the staging arrays
-    if (ct_tiles <= tmax && make_hp_layout(NR, 2, tmax, ct).total <= 113 * 1024) {  // logits stay resident
-      prm.chunk = ct * TK;
-      *handled = true;
-      // a third 32 KB ring slot when two CTAs per SM still fit (deeper loads in flight)
-      static const int hp_slots = env_int("SD_UMMA_HP_SLOTS", 3);
-      const bool three = hp_slots == 3 && make_hp_layout(NR, 3, tmax, ct).total <= 113 * 1024;
+  // K1 head packing: four kv heads per CTA (32-key tiles) while the critical list fits the
+  // TMEM-resident logits, else two heads per CTA (64-key tiles: twice the keys resident),
+  // else the clustered verify kernel over the gathered keys (SD_UMMA_HPC forces one packing)
+  static const int hpc_env = env_int("SD_UMMA_HPC", 0);
+  for (int HPC : {4, 2}) {
+    if (!hp_env || max_nq != 1 || kvp->dtype != SD_DTYPE_BF16 || kvp->head_dim != D || !(G == 4 || G == 8) ||
+        kvp->kv_heads % HPC != 0 || (hpc_env && hpc_env != HPC))
+      continue;
+    const int KPT = TK / HPC;
+    const int NQ = HPC * G, NR = NQ < 16 ? 16 : NQ, tmax = (256 - NR) / NR;
+    const int ct_tiles = (max(max_keys, 1) + KPT - 1) / KPT;  // KPT-key tiles
+    const int ct = (ct_tiles * KPT + TK - 1) / TK;           // 128-key units for the staging arrays
+    if (ct_tiles > tmax || make_hp_layout(NR, 2, tmax, ct).total > 113 * 1024) continue;  // logits stay resident
+    prm.chunk = ct * TK;
+    *handled = true;
+    // a third 32 KB ring slot when two CTAs per SM still fit (deeper loads in flight)
+    static const int hp_slots = env_int("SD_UMMA_HP_SLOTS", 3);
+    const bool three = hp_slots == 3 && make_hp_layout(NR, 3, tmax, ct).total <= 113 * 1024;
+    if (HPC == 2) {
       if (G == 4)
-        return three ? launch_hp<4, 4, 3, 256>(prm, num_items, kvp->kv_heads, ct, stream)
-                     : launch_hp<4, 4, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
-      return three ? launch_hp<8, 4, 3, 256>(prm, num_items, kvp->kv_heads, ct, stream)
-                   : launch_hp<8, 4, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
+        return three ? launch_hp<4, 2, 3, 256>(prm, num_items, kvp->kv_heads, ct, stream)
+                     : launch_hp<4, 2, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
+      return three ? launch_hp<8, 2, 3, 256>(prm, num_items, kvp->kv_heads, ct, stream)
+                   : launch_hp<8, 2, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
     }
+    if (G == 4)
+      return three ? launch_hp<4, 4, 3, 256>(prm, num_items, kvp->kv_heads, ct, stream)
+                   : launch_hp<4, 4, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
+    return three ? launch_hp<8, 4, 3, 256>(prm, num_items, kvp->kv_heads, ct, stream)
+                 : launch_hp<8, 4, 2, 256>(prm, num_items, kvp->kv_heads, ct, stream);
   }
   const int dense = (crit == nullptr && kvp->page_shift >= 4) ? 1 : 0;
   static const int tma_env = env_int("SD_K2_TMA", 1);

@@ -663,7 +663,8 @@ __host__ __device__ inline Layout make_hp_layout(int NR, int NSLOT, int TMAX, in
   o = align_up(o, 8);
   L.bar = o;   o += (2 * NSLOT + 2 * TMAX + 5) * 8;
   L.tptr = o;  o += 16;
-  L.wm = L.wl = L.xm = L.xl = L.rowlse = 0;
+  L.wm = o;    o += NSW * 8 * 2 * 4;     // 64-key heads: the two warps' (m, l) per q head
+  L.wl = L.xm = L.xl = L.rowlse = 0;
   L.total = align_up(o, 128) + 1024;
   return L;
 }
@@ -684,7 +685,7 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
   constexpr int TMAX = (TCOLS - NR) / NR;
   constexpr int OCOL = TMAX * NR;
   constexpr int WH = KPT >= 32 ? 1 : 32 / KPT;      // heads per warp (rows of a warp)
-  static_assert(KPT == 16 || KPT == 32, "head packing: 4 or 8 heads per CTA");
+  static_assert(KPT == 16 || KPT == 32 || KPT == 64, "head packing: 2, 4 or 8 heads per CTA");
 
   const int h0 = hgroup * HPC;
   const Item it = load_item(p.items, item_idx);
@@ -784,7 +785,9 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
       bool isv;
       fill_tile_hp(f, nt, TR, t, isv);
       const __nv_bfloat16* base = (isv ? Vg : Kg) + c * 8;
-      const int sl = sslot[t * KPT + (lane % KPT)];
+      // physical slots of the tile's keys: lane L holds key L (and L + 32 for 64-key heads)
+      const int sl = sslot[t * KPT + (lane % (KPT < 32 ? KPT : 32))];
+      const int sl_hi = KPT == 64 ? sslot[t * KPT + 32 + lane] : 0;
       if (f >= NSLOT) mbar_wait(empty + s, ((f / NSLOT) - 1) & 1);
       const uint32_t dst0 = ring_u + s * TILE_BYTES + (c >> 3) * (TK * 128);
 #pragma unroll
@@ -792,7 +795,8 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
         const int kk = pw * KK + k2;
         const int i = 2 * kk + sub;            // tile row = head-major (hh, key)
         const int hh = (2 * kk) / KPT;         // same for both rows of the instruction
-        const int slot = __shfl_sync(0xffffffffu, sl, ((2 * kk) % KPT) + sub);
+        const int kin = (2 * kk) % KPT;          // even: both rows' keys lie in one 32-key half
+        const int slot = __shfl_sync(0xffffffffu, KPT == 64 && kin >= 32 ? sl_hi : sl, (kin & 31) + sub);
         cp_async16(dst0 + i * 128 + (((c & 7) ^ (i & 7)) << 4), base + (int64_t)slot * row_stride + hh * D, pol);
       }
       cp_async_mbar_arrive(full + s);
@@ -906,17 +910,29 @@ __device__ __forceinline__ void draft_body(const Params& p, const int hgroup, co
       }
     }
   }
-  // statistics of each (head, q head) row: reduce over the KPT lanes of this head
+  // statistics of each (head, q head) row: reduce over the KPT keys of this head (the warp's
+  // lanes; a 64-key head also merges its partner warp's half through shared memory)
   float lse[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
 #pragma unroll
-    for (int o = KPT / 2; o >= 1; o >>= 1) {
+    for (int o = (KPT < 32 ? KPT : 32) / 2; o >= 1; o >>= 1) {
       const float om = __shfl_xor_sync(0xffffffffu, m[g], o), ol = __shfl_xor_sync(0xffffffffu, l[g], o);
       stat_merge(m[g], l[g], om, ol);
     }
-    lse[g] = m[g] + log2f(l[g]);
   }
+  if constexpr (KPT == 64) {
+    float* xs = reinterpret_cast<float*>(smem + L.wm);  // [warp][G][m, l]
+    if (lane == 0) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) xs[(warp * G + g) * 2] = m[g], xs[(warp * G + g) * 2 + 1] = l[g];
+    }
+    sw_bar();
+#pragma unroll
+    for (int g = 0; g < G; ++g) stat_merge(m[g], l[g], xs[((warp ^ 1) * G + g) * 2], xs[((warp ^ 1) * G + g) * 2 + 1]);
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) lse[g] = m[g] + log2f(l[g]);
   if (tid == 0) {
     HTRACE(2, gtime());
     HTRACE(3, gtime());

@@ -141,10 +141,14 @@ def test_sparse_draft_attention_matches_oracle(dtype, force_generic, d):
     assert np.abs(lse.double().cpu().numpy() - rl).max() <= tol
 
 
-@pytest.mark.parametrize("G,use_planted", [(4, True), (8, False), (8, True)])
-def test_draft_attention_head_packed_bf16(G, use_planted):
-    """Draft items of several requests (4 kv heads per CTA, block-diagonal P): outputs and
-    lse per request vs the oracle over critical U fresh U self, with the planted bias."""
+@pytest.mark.parametrize("G,use_planted,buds", [(4, True, (37, 130, 200)), (8, False, (37, 130, 200)),
+                                                (8, True, (37, 130, 200)), (4, True, (300, 700, 900)),
+                                                (8, False, (250, 500, 900))])
+def test_draft_attention_head_packed_bf16(G, use_planted, buds):
+    """Draft items of several requests (kv heads packed per CTA, block-diagonal P): outputs and
+    lse per request vs the oracle over critical U fresh U self, with the planted bias. The
+    larger budgets exceed the 4-head packing's resident logits and take the 2-head, 64-key-tile
+    variant."""
     rng = np.random.default_rng(20 + G)
     Hkv, d, B = 8, 128, 3
     Hq = Hkv * G
@@ -152,11 +156,10 @@ def test_draft_attention_head_packed_bf16(G, use_planted):
     pool = _pool(1, Hkv, d, n0 + 4, B, torch.bfloat16, shuffle_seed=7)
     for r in range(B):
         _fill(pool, r, n0 + 4, rng)
-    buds = [37, 130, 200]
     js = [0, 1, 3]
     crit = [np.sort(rng.choice(n0, size=b, replace=False)).astype(np.int32) for b in buds]
     planted = np.array(sorted(set(int(x) for x in crit[1][:3]) | {n0 + 1}), dtype=np.int32)
-    offs = np.cumsum([0] + buds)
+    offs = np.cumsum([0] + list(buds))
     crit_dev = torch.from_numpy(np.concatenate(crit)).to(DEV)
     q = torch.from_numpy(rng.normal(size=(B, Hq, d))).to(DEV, torch.bfloat16)
     out = torch.empty_like(q)

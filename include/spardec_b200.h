@@ -223,7 +223,10 @@ typedef struct sd_attn_launch {
  * high-priority stream, the draft launch on a low-priority one (forked from / joined
  * into `stream`), unless flags bit 0 is set or attn_events is given.
  * attn_events (nullable): cudaEvent_t pairs [layers][num_launches][2] recorded around
- * each attention launch (launches then run one after another). */
+ * each attention launch (launches then run one after another).
+ * flags bit 1: f3 fused verify + draft launch (sd_attention_pair); bit 3: the whole loop
+ * is captured and launched as one CUDA graph (a cached executable updated in place each
+ * call; falls back to direct launches when the capture is not possible). */
 int sd_forward_layers(const sd_layer_weights* weights, int32_t layers, float* x, void* hn, void* qkv, void* q,
                       void* ctx, void* hm, int32_t rows, int32_t hidden, int32_t q_heads,
                       const int32_t* row_table, const int32_t* row_pos, const sd_paged_kv* kv,
@@ -247,6 +250,10 @@ int sd_attention_pair(const void* q, void* out, const sd_paged_kv* kv, int32_t l
  * c_f32 else bf16, beta 0 (overwrite) or 1 (accumulate). */
 int sd_linear(const void* A, const void* W, void* C, int32_t R, int32_t N, int32_t K, int32_t c_f32, float beta,
               void* stream);
+
+/* CUDA-graph path of sd_forward_layers on this thread and device: which 0 = executable
+ * graphs instantiated, 1 = in-place updates (topology unchanged since the last call). */
+int64_t sd_forward_graph_stats(int32_t which);
 
 /* Workspace sd_forward_layers needs: the attention launches' (sd_attention_workspace_bytes,
  * max over the launches) plus a RoPE cos/sin table of `rows` rows kept at its end. */

@@ -74,6 +74,7 @@ SIGNATURES = {
                                        _c_p, ctypes.c_int64, _c_p]),
     "sd_step_commit": (ctypes.c_int, [_c_p, _i32, _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
     "sd_rmsnorm_cast": (ctypes.c_int, [_c_p, _i32, _i32, ctypes.c_float, _c_p, _i32, _c_p]),
+    "sd_forward_graph_stats": (_i64, [_i32]),
     "sd_forward_layers": (ctypes.c_int, [ctypes.POINTER(LayerWeights), _i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                                          _i32, _i32, _i32, _c_p, _c_p, ctypes.POINTER(PagedKvDesc),
                                          ctypes.POINTER(AttnLaunchDesc), _i32, _c_p, _i32, ctypes.c_float,

@@ -18,6 +18,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
 
 #include "common.cuh"
 
@@ -29,6 +30,7 @@ extern "C" int sd_rope_kv_write(const void* qkv, int64_t qkv_row_stride, int32_t
 extern "C" int sd_attention_pair(const void* q, void* out, const sd_paged_kv* kv, int32_t layer,
                                  const sd_attn_launch* verify, const sd_attn_launch* draft, const int32_t* planted,
                                  int32_t num_planted, float planted_bonus, int32_t q_heads, float scale, void* stream);
+extern "C" int64_t sd_launch_count(void);
 extern "C" int sd_attention(const void* q, void* out, float* lse, const sd_paged_kv* kv, int32_t layer,
                             const int32_t* items, int32_t num_items, int32_t max_keys, int32_t max_nq,
                             const int32_t* crit, uint64_t* acc, int64_t acc_row_stride, int32_t acc_shift,
@@ -179,32 +181,49 @@ static LtPlan lt_tune(LtState* st, int Rb, int N, int K, bool c_f32, float beta,
   return plan;
 }
 
-static int gemm(cublasHandle_t hd, int R, int N, int K, const void* A, const void* Wt, void* C, bool c_f32,
-                float beta) {
-  const float alpha = 1.f;
+static int gemm_tune_enabled() {
   static const int tune = [] {
     const char* v = getenv("SD_GEMM_TUNE");
     return v && *v ? atoi(v) : 1;
   }();
-  if (tune) {
-    LtState* st = lt_state();
-    cudaStream_t s = nullptr;
-    cublasGetStream(hd, &s);
-    if (st != nullptr && st->ws != nullptr) {
-      const int Rb = (R + 15) / 16 * 16;
-      const auto key = std::make_tuple(Rb, N, K, c_f32 ? 1 : 0, beta != 0.f ? 1 : 0);
-      auto it = st->plans.find(key);
-      if (it == st->plans.end()) it = st->plans.emplace(key, lt_tune(st, Rb, N, K, c_f32, beta, s)).first;
-      if (it->second.valid) {
-        LtCall call;
-        cublasLtMatmulHeuristicResult_t chk;
-        if (call.init(R, N, K, c_f32) &&
-            cublasLtMatmulAlgoCheck(st->lt, call.op, call.la, call.lb, call.lc, call.lc, &it->second.algo, &chk) ==
-                CUBLAS_STATUS_SUCCESS &&
-            cublasLtMatmul(st->lt, call.op, &alpha, Wt, call.la, A, call.lb, &beta, C, call.lc, C, call.lc,
-                           &it->second.algo, st->ws, st->ws_bytes, s) == CUBLAS_STATUS_SUCCESS)
-          return 0;
-      }
+  return tune;
+}
+
+// the tuned plan of one GEMM shape, created on first use (tuning synchronises: never
+// inside a stream capture, see gemm_prepare)
+static const LtPlan* gemm_plan(cublasHandle_t hd, int R, int N, int K, bool c_f32, float beta) {
+  LtState* st = lt_state();
+  if (st == nullptr || st->ws == nullptr) return nullptr;
+  cudaStream_t s = nullptr;
+  cublasGetStream(hd, &s);
+  const int Rb = (R + 15) / 16 * 16;
+  const auto key = std::make_tuple(Rb, N, K, c_f32 ? 1 : 0, beta != 0.f ? 1 : 0);
+  auto it = st->plans.find(key);
+  if (it == st->plans.end()) it = st->plans.emplace(key, lt_tune(st, Rb, N, K, c_f32, beta, s)).first;
+  return &it->second;
+}
+
+static void gemm_prepare(cublasHandle_t hd, int R, int N, int K, bool c_f32, float beta) {
+  if (gemm_tune_enabled()) gemm_plan(hd, R, N, K, c_f32, beta);
+}
+
+static int gemm(cublasHandle_t hd, int R, int N, int K, const void* A, const void* Wt, void* C, bool c_f32,
+                float beta) {
+  const float alpha = 1.f;
+  if (gemm_tune_enabled()) {
+    const LtPlan* plan = gemm_plan(hd, R, N, K, c_f32, beta);
+    if (plan != nullptr && plan->valid) {
+      LtState* st = lt_state();
+      cudaStream_t s = nullptr;
+      cublasGetStream(hd, &s);
+      LtCall call;
+      cublasLtMatmulHeuristicResult_t chk;
+      if (call.init(R, N, K, c_f32) &&
+          cublasLtMatmulAlgoCheck(st->lt, call.op, call.la, call.lb, call.lc, call.lc, &plan->algo, &chk) ==
+              CUBLAS_STATUS_SUCCESS &&
+          cublasLtMatmul(st->lt, call.op, &alpha, Wt, call.la, A, call.lb, &beta, C, call.lc, C, call.lc, &plan->algo,
+                         st->ws, st->ws_bytes, s) == CUBLAS_STATUS_SUCCESS)
+        return 0;
     }
   }
   const cublasStatus_t st =
@@ -264,19 +283,37 @@ extern "C" int64_t sd_forward_workspace_bytes(int32_t rows, int32_t head_dim, in
   return ((attention_bytes + 255) / 256) * 256 + sd::rope_table_bytes(rows, head_dim) + 256;  // + alignment slack
 }
 
-extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, float* x, void* hn, void* qkv, void* q,
-                                 void* ctx, void* hm, int32_t rows, int32_t hidden, int32_t q_heads,
-                                 const int32_t* row_table, const int32_t* row_pos, const sd_paged_kv* kv,
-                                 const sd_attn_launch* launches, int32_t num_launches, const int32_t* planted,
-                                 int32_t num_planted, float planted_bonus, float scale, float eps, void* workspace,
-                                 int64_t workspace_bytes, void* const* attn_events, int32_t flags, void* stream) {
-  SD_REQUIRE(w != nullptr && x != nullptr && kv != nullptr, "sd_forward_layers: null pointer");
-  SD_REQUIRE(kv->dtype == SD_DTYPE_BF16, "sd_forward_layers: bf16 pools only (fp32 parity mode runs in torch)");
-  SD_REQUIRE(rows > 0 && layers > 0 && num_launches >= 0, "sd_forward_layers: bad sizes");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cublasHandle_t hd = sd::handle_for_thread();
-  SD_REQUIRE(hd != nullptr, "sd_forward_layers: cublasCreate failed");
-  cublasSetStream(hd, s);
+namespace {
+// everything one forward issues on stream s (and the two attention side streams)
+struct LayerLoop {
+  const sd_layer_weights* w;
+  int32_t layers;
+  float* x;
+  void *hn, *qkv, *q, *ctx, *hm;
+  int32_t rows, hidden, q_heads;
+  const int32_t *row_table, *row_pos;
+  const sd_paged_kv* kv;
+  const sd_attn_launch* launches;
+  int32_t num_launches;
+  const int32_t* planted;
+  int32_t num_planted;
+  float planted_bonus, scale, eps;
+  void* workspace;
+  int64_t workspace_bytes;
+  void* const* attn_events;
+  int32_t flags;
+  void* stream;
+};
+
+int issue_layers(const LayerLoop& a, cublasHandle_t hd) {
+  cudaStream_t s = static_cast<cudaStream_t>(a.stream);
+  void* stream = a.stream;
+  const sd_paged_kv* kv = a.kv;
+  const sd_attn_launch* launches = a.launches;
+  const int num_launches = a.num_launches, rows = a.rows, hidden = a.hidden, q_heads = a.q_heads;
+  float* x = a.x;
+  void* workspace = a.workspace;
+  int64_t workspace_bytes = a.workspace_bytes;
   const int qkv_w = (q_heads + 2 * kv->kv_heads) * kv->head_dim;
   const int64_t hm_n = (int64_t)rows * 2 * hidden;
   const int tanh_blocks = (int)std::min<int64_t>((hm_n / 8 + 255) / 256 + 1, 148 * 8);
@@ -292,29 +329,32 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
   if (use_table) {
     workspace_bytes = (int64_t)(tab0 - ws0);
     table = reinterpret_cast<float2*>(tab0);
-    sd::rope_table(row_pos, rows, kv->head_dim, table, s);
+    sd::rope_table(a.row_pos, rows, kv->head_dim, table, s);
   }
   // two attention launches (verify + draft) overlap on priority streams unless timed per
   // launch (attn_events) or disabled (flags bit 0)
   sd::AttnStreams* as = nullptr;
-  const bool overlap = num_launches == 2 && attn_events == nullptr && !(flags & 1) &&
+  const bool overlap = num_launches == 2 && a.attn_events == nullptr && !(a.flags & 1) &&
                        launches[0].num_items > 0 && launches[1].num_items > 0 && (as = sd::attn_streams()) != nullptr;
   // f3 fused verify + draft launch (flags bit 1): launch 0 dense verify, launch 1 drafts
-  const bool fused = (flags & 2) && num_launches == 2 && attn_events == nullptr && launches[0].num_items > 0 &&
+  const bool fused = (a.flags & 2) && num_launches == 2 && a.attn_events == nullptr && launches[0].num_items > 0 &&
                      launches[1].num_items > 0 && launches[0].crit == nullptr && launches[1].crit != nullptr &&
                      launches[1].max_nq == 1;
+  const void* q = a.q;
+  void* ctx = a.ctx;
   int rc;
-  for (int l = 0; l < layers; ++l) {
-    if ((rc = sd_rmsnorm_cast(x, rows, hidden, eps, hn, SD_DTYPE_BF16, stream)) != 0) return rc;
-    if ((rc = sd::gemm(hd, rows, qkv_w, hidden, hn, w[l].w_qkv, qkv, false, 0.f)) != 0) return rc;
+  for (int l = 0; l < a.layers; ++l) {
+    const sd_layer_weights& wl = a.w[l];
+    if ((rc = sd_rmsnorm_cast(x, rows, hidden, a.eps, a.hn, SD_DTYPE_BF16, stream)) != 0) return rc;
+    if ((rc = sd::gemm(hd, rows, qkv_w, hidden, a.hn, wl.w_qkv, a.qkv, false, 0.f)) != 0) return rc;
     if (use_table)
-      sd::rope_kv_write_table(qkv, qkv_w, rows, row_table, row_pos, kv, l, q_heads, table, q, s);
-    else if ((rc = sd_rope_kv_write(qkv, qkv_w, rows, row_table, row_pos, kv, l, q_heads, q, stream)) != 0)
+      sd::rope_kv_write_table(a.qkv, qkv_w, rows, a.row_table, a.row_pos, kv, l, q_heads, table, a.q, s);
+    else if ((rc = sd_rope_kv_write(a.qkv, qkv_w, rows, a.row_table, a.row_pos, kv, l, q_heads, a.q, stream)) != 0)
       return rc;
     if (fused) {
       // f3: one launch, the verify grid's CTAs take the draft units after their verify chunk
-      rc = sd_attention_pair(q, ctx, kv, l, &launches[0], &launches[1], planted, num_planted, planted_bonus, q_heads,
-                             scale, stream);
+      rc = sd_attention_pair(q, ctx, kv, l, &launches[0], &launches[1], a.planted, a.num_planted, a.planted_bonus,
+                             q_heads, a.scale, stream);
       if (rc == 0) goto attn_done;
       if (rc != 1) return rc;
     }
@@ -323,10 +363,10 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
       cudaEventRecord(as->fork, s);
       cudaStreamWaitEvent(as->hi, as->fork, 0);
       cudaStreamWaitEvent(as->lo, as->fork, 0);
-      if ((rc = attn_launch(launches[0], q, ctx, kv, l, planted, num_planted, planted_bonus, q_heads, scale,
+      if ((rc = attn_launch(launches[0], q, ctx, kv, l, a.planted, a.num_planted, a.planted_bonus, q_heads, a.scale,
                             workspace, workspace_bytes, as->hi)) != 0)
         return rc;
-      if ((rc = attn_launch(launches[1], q, ctx, kv, l, planted, num_planted, planted_bonus, q_heads, scale,
+      if ((rc = attn_launch(launches[1], q, ctx, kv, l, a.planted, a.num_planted, a.planted_bonus, q_heads, a.scale,
                             workspace, workspace_bytes, as->lo)) != 0)
         return rc;
       cudaEventRecord(as->join_hi, as->hi);
@@ -335,27 +375,196 @@ extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, floa
       cudaStreamWaitEvent(s, as->join_lo, 0);
     } else {
       for (int i = 0; i < num_launches; ++i) {
-        const sd_attn_launch& a = launches[i];
-        if (a.num_items == 0) continue;
-        cudaEvent_t* ev = attn_events ? (cudaEvent_t*)(attn_events + 2 * ((int64_t)l * num_launches + i)) : nullptr;
+        const sd_attn_launch& al = launches[i];
+        if (al.num_items == 0) continue;
+        cudaEvent_t* ev =
+            a.attn_events ? (cudaEvent_t*)(a.attn_events + 2 * ((int64_t)l * num_launches + i)) : nullptr;
         if (ev && ev[0]) cudaEventRecord(ev[0], s);
-        if ((rc = attn_launch(a, q, ctx, kv, l, planted, num_planted, planted_bonus, q_heads, scale, workspace,
-                              workspace_bytes, s)) != 0)
+        if ((rc = attn_launch(al, q, ctx, kv, l, a.planted, a.num_planted, a.planted_bonus, q_heads, a.scale,
+                              workspace, workspace_bytes, s)) != 0)
           return rc;
         if (ev && ev[1]) cudaEventRecord(ev[1], s);
       }
     }
   attn_done:
-    if ((rc = sd::gemm(hd, rows, hidden, hidden, ctx, w[l].wo, x, true, 1.f)) != 0) return rc;
-    if ((rc = sd_rmsnorm_cast(x, rows, hidden, eps, hn, SD_DTYPE_BF16, stream)) != 0) return rc;
-    if ((rc = sd::gemm(hd, rows, 2 * hidden, hidden, hn, w[l].mlp_in, hm, false, 0.f)) != 0) return rc;
-    sd::tanh_bf16_kernel<<<tanh_blocks, 256, 0, s>>>(static_cast<__nv_bfloat16*>(hm), hm_n);
+    if ((rc = sd::gemm(hd, rows, hidden, hidden, ctx, wl.wo, x, true, 1.f)) != 0) return rc;
+    if ((rc = sd_rmsnorm_cast(x, rows, hidden, a.eps, a.hn, SD_DTYPE_BF16, stream)) != 0) return rc;
+    if ((rc = sd::gemm(hd, rows, 2 * hidden, hidden, a.hn, wl.mlp_in, a.hm, false, 0.f)) != 0) return rc;
+    sd::tanh_bf16_kernel<<<tanh_blocks, 256, 0, s>>>(static_cast<__nv_bfloat16*>(a.hm), hm_n);
     sd::count_launch();
-    if ((rc = sd::gemm(hd, rows, hidden, 2 * hidden, hm, w[l].mlp_out, x, true, 1.f)) != 0) return rc;
+    if ((rc = sd::gemm(hd, rows, hidden, 2 * hidden, a.hm, wl.mlp_out, x, true, 1.f)) != 0) return rc;
   }
   // the workspace is handed back zero-filled (the attention launches rely on it)
   if (use_table) cudaMemsetAsync(table, 0, table_bytes, s);
+  return 0;
+}
+
+// The forward as one CUDA graph (flags bit 3): the layer loop is captured on the caller's
+// stream (side streams join the capture through the fork / join events), the capture is
+// applied to a cached executable graph with cudaGraphExecUpdate (same topology: only
+// kernel parameters and grids changed since the last iteration; re-instantiated when
+// the topology changed), and launched.  Two executables alternate so an update never
+// touches the one the previous, possibly still running, iteration launched.  The host
+// cost is the capture (~ the eager enqueue) + the update; the device runs the ~300
+// launches without per-launch front-end gaps.
+struct GraphCache {
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  std::vector<unsigned> sig[2];  // cluster shape of every kernel node of the executable
+  int next = 0;
+  int64_t instantiations = 0, updates = 0;
+  // captured and launched on an own stream (the caller's may be the legacy default stream,
+  // which cannot be captured), ordered after / before the caller's work by events
+  cudaStream_t cs = nullptr;
+  cudaEvent_t in = nullptr, out = nullptr;
+};
+GraphCache* graph_cache() {
+  constexpr int kMaxDev = 16;
+  static thread_local GraphCache gc[kMaxDev];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  return &gc[dev];
+}
+
+// 0: launched as a graph; 1: capture not possible (caller runs the loop eagerly); < 0 error
+int launch_as_graph(const LayerLoop& a, cublasHandle_t hd) {
+  GraphCache* gc = graph_cache();
+  if (gc == nullptr) return 1;
+  if (gc->cs == nullptr) {
+    if (cudaStreamCreateWithFlags(&gc->cs, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&gc->in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&gc->out, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      gc->cs = nullptr;
+      return 1;
+    }
+  }
+  cudaStream_t caller = static_cast<cudaStream_t>(a.stream);
+  cudaStream_t s = gc->cs;
+  LayerLoop ac = a;
+  ac.stream = s;
+  // every cuBLASLt plan this forward needs is tuned before the capture (tuning synchronises)
+  const int qkv_w = (a.q_heads + 2 * a.kv->kv_heads) * a.kv->head_dim;
+  sd::gemm_prepare(hd, a.rows, qkv_w, a.hidden, false, 0.f);
+  sd::gemm_prepare(hd, a.rows, a.hidden, a.hidden, true, 1.f);
+  sd::gemm_prepare(hd, a.rows, 2 * a.hidden, a.hidden, false, 0.f);
+  sd::gemm_prepare(hd, a.rows, a.hidden, 2 * a.hidden, true, 1.f);
+  if (sd::attn_streams() == nullptr) return 1;
+  cudaGetLastError();
+  // the capture stream waits for the caller's prior work (outside the capture)
+  cudaEventRecord(gc->in, caller);
+  cudaStreamWaitEvent(s, gc->in, 0);
+  cublasSetStream(hd, s);
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    cublasSetStream(hd, caller);
+    return 1;
+  }
+  const int64_t launches0 = sd_launch_count();
+  const int rc = issue_layers(ac, hd);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(s, &g);
+  cublasSetStream(hd, caller);
+  if (rc != 0 || ce != cudaSuccess || g == nullptr) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    sd::count_launch(-(int)(sd_launch_count() - launches0));  // nothing of the capture ran
+    return rc < 0 ? rc : 1;
+  }
+  // an in-place update keeps the executable's launch attributes: the cluster shape of every
+  // kernel node (the K2 planner's cluster size varies with the context) must match
+  std::vector<unsigned> sig;
+  {
+    size_t n = 0;
+    cudaGraphGetNodes(g, nullptr, &n);
+    std::vector<cudaGraphNode_t> nodes(n);
+    cudaGraphGetNodes(g, nodes.data(), &n);
+    sig.reserve(n);
+    for (size_t i = 0; i < n; ++i) {
+      cudaGraphNodeType t;
+      cudaGraphNodeGetType(nodes[i], &t);
+      unsigned v = 0xffffffffu;
+      if (t == cudaGraphNodeTypeKernel) {
+        cudaLaunchAttributeValue av{};
+        v = cudaGraphKernelNodeGetAttribute(nodes[i], cudaLaunchAttributeClusterDimension, &av) == cudaSuccess
+                ? av.clusterDim.x * 65536u + av.clusterDim.y * 256u + av.clusterDim.z
+                : 0u;
+      }
+      sig.push_back(v);
+    }
+    cudaGetLastError();
+  }
+  static const int allow_update = [] {
+    const char* v = getenv("SD_GRAPH_UPDATE");
+    return v && *v ? atoi(v) : 1;
+  }();
+  const int slot = gc->next;
+  cudaGraphExec_t& ex = gc->exec[slot];
+  gc->next ^= 1;
+  if (ex != nullptr && (!allow_update || gc->sig[slot] != sig)) {
+    cudaGraphExecDestroy(ex);
+    ex = nullptr;
+  }
+  if (ex != nullptr) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(ex, g, &info) == cudaSuccess) {
+      ++gc->updates;
+    } else {
+      cudaGetLastError();
+      cudaGraphExecDestroy(ex);
+      ex = nullptr;
+    }
+  }
+  if (ex == nullptr) {
+    if (cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) {
+      cudaGetLastError();
+      ex = nullptr;
+      cudaGraphDestroy(g);
+      sd::count_launch(-(int)(sd_launch_count() - launches0));  // nothing of the capture ran
+      return 1;
+    }
+    ++gc->instantiations;
+    gc->sig[slot] = std::move(sig);
+  }
+  cudaGraphDestroy(g);
+  if (cudaGraphLaunch(ex, s) != cudaSuccess) {
+    sd::set_error("sd_forward_layers: cudaGraphLaunch failed");
+    return -1;
+  }
+  // the caller's later work waits for the graph
+  cudaEventRecord(gc->out, s);
+  cudaStreamWaitEvent(caller, gc->out, 0);
+  return 0;
+}
+}  // namespace
+
+extern "C" int sd_forward_layers(const sd_layer_weights* w, int32_t layers, float* x, void* hn, void* qkv, void* q,
+                                 void* ctx, void* hm, int32_t rows, int32_t hidden, int32_t q_heads,
+                                 const int32_t* row_table, const int32_t* row_pos, const sd_paged_kv* kv,
+                                 const sd_attn_launch* launches, int32_t num_launches, const int32_t* planted,
+                                 int32_t num_planted, float planted_bonus, float scale, float eps, void* workspace,
+                                 int64_t workspace_bytes, void* const* attn_events, int32_t flags, void* stream) {
+  SD_REQUIRE(w != nullptr && x != nullptr && kv != nullptr, "sd_forward_layers: null pointer");
+  SD_REQUIRE(kv->dtype == SD_DTYPE_BF16, "sd_forward_layers: bf16 pools only (fp32 parity mode runs in torch)");
+  SD_REQUIRE(rows > 0 && layers > 0 && num_launches >= 0, "sd_forward_layers: bad sizes");
+  cublasHandle_t hd = sd::handle_for_thread();
+  SD_REQUIRE(hd != nullptr, "sd_forward_layers: cublasCreate failed");
+  cublasSetStream(hd, static_cast<cudaStream_t>(stream));
+  const LayerLoop a{w,        layers,          x,         hn,      qkv,         q,          ctx,
+                    hm,       rows,            hidden,    q_heads, row_table,   row_pos,    kv,
+                    launches, num_launches,    planted,   num_planted, planted_bonus, scale, eps,
+                    workspace, workspace_bytes, attn_events, flags, stream};
+  int rc = 1;
+  // flags bit 3: one CUDA graph for the whole loop (not with per-launch timing events)
+  if ((flags & 8) && attn_events == nullptr) rc = launch_as_graph(a, hd);
+  if (rc == 1) rc = issue_layers(a, hd);
+  if (rc != 0) return rc;
   SD_CUDA_RETURN();
+}
+
+extern "C" int64_t sd_forward_graph_stats(int32_t which) {
+  GraphCache* gc = graph_cache();
+  if (gc == nullptr) return -1;
+  return which == 0 ? gc->instantiations : gc->updates;
 }
 
 // One linear layer through the same tuned path (the LM head of the batched forward):

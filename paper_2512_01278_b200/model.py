@@ -324,6 +324,9 @@ NATIVE_FORWARD = True  # bf16: the layer loop runs in the library (sd_forward_la
 OVERLAP_ATTENTION = os.environ.get("SD_ATTN_OVERLAP", "1") == "1"
 # f3: verify and draft work of a layer in ONE launch (csrc/attn_umma.cu launch_attn_pair)
 FUSED_ATTENTION = os.environ.get("SD_ATTN_FUSED", "0") == "1"
+# the native layer loop captured and launched as one CUDA graph (csrc/forward.cu
+# launch_as_graph: cached executable updated in place per call) unless SD_FORWARD_GRAPH=0
+FORWARD_GRAPH = os.environ.get("SD_FORWARD_GRAPH", "1") == "1"
 # query rows (tokens x GQA group) per attention work item for multi-token windows (prefill,
 # forward_full): <= 48 keeps the tcgen05 verify kernel at two CTAs per SM
 ITEM_ROWS = 48
@@ -379,7 +382,7 @@ def _forward_native(model: ToyModel, pool: PagedKvPool, tokens, row_table, row_p
             for l, (e0, e1) in enumerate(ln.events):
                 ev_arr[2 * (l * len(launches) + i)] = e0.cuda_event
                 ev_arr[2 * (l * len(launches) + i) + 1] = e1.cuda_event
-    flags = (0 if OVERLAP_ATTENTION else 1) | (2 if FUSED_ATTENTION else 0)
+    flags = (0 if OVERLAP_ATTENTION else 1) | (2 if FUSED_ATTENTION else 0) | (8 if FORWARD_GRAPH else 0)
     N.check(lib.sd_forward_layers(wts, c.num_layers, x.data_ptr(), hn.data_ptr(), qkv.data_ptr(), q.data_ptr(),
                                   ctx.data_ptr(), hm.data_ptr(), R, h, Hq, row_table.data_ptr(), row_pos.data_ptr(),
                                   ctypes.byref(desc), descs, len(launches), N.ptr(model.planted_dev), n_planted,

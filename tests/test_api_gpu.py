@@ -195,3 +195,54 @@ def test_native_layer_loop_matches_python_loop_bf16(planted):
     assert (ln - lp).abs().max().item() <= 2e-2 * max(1.0, scale)
     assert (an - ap).abs().max().item() <= 2e-2 * 16
     assert (kn - kp).abs().max().item() <= 2e-2 * max(1.0, kp.abs().max().item())
+
+
+def test_forward_graph_equals_direct_launches_bf16():
+    """The CUDA-graph path of the native layer loop (csrc/forward.cu launch_as_graph: capture,
+    in-place update of a cached executable, re-instantiation when a kernel's cluster shape
+    changes) gives bitwise the direct launches' results over a sequence of calls whose K2
+    plans differ (contexts 300 / 6000 / 300 / 2500 rows: different cluster sizes)."""
+    from paper_2512_01278_b200 import _native as N
+    from paper_2512_01278_b200.model import AttnLaunch, forward_rows, lm_head, make_items
+    from paper_2512_01278_b200.paged import PagedKvPool
+
+    cfg = M.ModelConfig(2, 16, 4, 128, 1024, seed=9)
+    model = M.init_model(cfg, dtype=torch.bfloat16)
+    dev = model.device
+    lib = N.load_library()
+    results = {}
+    for graph in (False, True):
+        pool = PagedKvPool(cfg.num_layers, cfg.num_kv_heads, cfg.head_dim, 100, 128, 2, 64, torch.bfloat16, dev)
+        for r in range(2):
+            pool.ensure_tokens(r, 6100)
+        pool.sync_table()
+        g = torch.Generator(device=dev).manual_seed(3)
+        pool.k.copy_(torch.randn(pool.k.shape, generator=g, device=dev))
+        pool.v.copy_(torch.randn(pool.v.shape, generator=g, device=dev))
+        rng = np.random.default_rng(4)
+        old = M.FORWARD_GRAPH
+        M.FORWARD_GRAPH = graph
+        inst0, upd0 = lib.sd_forward_graph_stats(0), lib.sd_forward_graph_stats(1)
+        outs = []
+        try:
+            for n0 in (300, 6000, 300, 2500, 2500):
+                toks = torch.tensor(rng.integers(0, 1024, 6), dtype=torch.int32, device=dev)
+                rt = torch.tensor([0] * 5 + [1], dtype=torch.int32, device=dev)
+                rp = torch.tensor([n0 + i for i in range(5)] + [n0 + 2], dtype=torch.int32, device=dev)
+                crit = torch.tensor(sorted(rng.choice(n0, 20, replace=False).tolist()), dtype=torch.int32, device=dev)
+                acc = torch.zeros(5, n0 + 8, dtype=torch.int64, device=dev)
+                launches = [AttnLaunch(make_items([(0, 0, 5, n0, 0, 0, 0, 0, 1)], dev), 1, n0 + 5, 5, acc=acc,
+                                       acc_row_stride=n0 + 8, acc_shift=40),
+                            AttnLaunch(make_items([(1, 5, 1, n0 + 2, 0, 20, n0, -1, 0)], dev), 1, 23, 1, crit=crit)]
+                x = forward_rows(model, pool, toks, rt, rp, launches)
+                logits = lm_head(model, x)
+                torch.cuda.synchronize()
+                outs.append((logits.float().cpu(), acc.cpu()))
+        finally:
+            M.FORWARD_GRAPH = old
+        results[graph] = outs
+        if graph:
+            assert lib.sd_forward_graph_stats(0) + lib.sd_forward_graph_stats(1) - inst0 - upd0 == 5
+    for (la, aa), (lb, ab) in zip(results[False], results[True]):
+        assert torch.equal(la, lb)
+        assert torch.equal(aa, ab)

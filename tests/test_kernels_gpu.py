@@ -141,16 +141,17 @@ def test_sparse_draft_attention_matches_oracle(dtype, force_generic, d):
     assert np.abs(lse.double().cpu().numpy() - rl).max() <= tol
 
 
-@pytest.mark.parametrize("G,use_planted,buds", [(4, True, (37, 130, 200)), (8, False, (37, 130, 200)),
-                                                (8, True, (37, 130, 200)), (4, True, (300, 700, 900)),
-                                                (8, False, (250, 500, 900))])
-def test_draft_attention_head_packed_bf16(G, use_planted, buds):
+@pytest.mark.parametrize("G,use_planted,buds,Hkv", [(4, True, (37, 130, 200), 8), (8, False, (37, 130, 200), 8),
+                                                    (8, True, (37, 130, 200), 8), (4, True, (300, 700, 900), 8),
+                                                    (8, False, (250, 500, 900), 8), (4, False, (10, 26, 29), 2),
+                                                    (8, True, (5, 20, 60), 8), (4, True, (3, 300, 900), 2)])
+def test_draft_attention_head_packed_bf16(G, use_planted, buds, Hkv):
     """Draft items of several requests (kv heads packed per CTA, block-diagonal P): outputs and
     lse per request vs the oracle over critical U fresh U self, with the planted bias. The
     larger budgets exceed the 4-head packing's resident logits and take the 2-head, 64-key-tile
     variant."""
     rng = np.random.default_rng(20 + G)
-    Hkv, d, B = 8, 128, 3
+    d, B = 128, 3
     Hq = Hkv * G
     n0 = 2000
     pool = _pool(1, Hkv, d, n0 + 4, B, torch.bfloat16, shuffle_seed=7)
@@ -162,13 +163,16 @@ def test_draft_attention_head_packed_bf16(G, use_planted, buds):
     offs = np.cumsum([0] + list(buds))
     crit_dev = torch.from_numpy(np.concatenate(crit)).to(DEV)
     q = torch.from_numpy(rng.normal(size=(B, Hq, d))).to(DEV, torch.bfloat16)
-    out = torch.empty_like(q)
-    lse = torch.empty(B, Hq, dtype=torch.float32, device=DEV)
+    # one sentinel row past the outputs: no write may land outside the items' rows
+    out_all = torch.full((B + 1, Hq, d), 7.0, dtype=torch.bfloat16, device=DEV)
+    lse_all = torch.full((B + 1, Hq), 7.0, dtype=torch.float32, device=DEV)
+    out, lse = out_all[:B], lse_all[:B]
     items = make_items([(r, r, 1, n0 + js[r], int(offs[r]), buds[r], n0, -1, 0) for r in range(B)], DEV)
     K.attention(q, out, pool, 0, items, B, max(b + j + 1 for b, j in zip(buds, js)), 1, Hq, crit=crit_dev, lse=lse,
                 planted=torch.from_numpy(planted).to(DEV) if use_planted else None,
                 planted_bonus=2.5 if use_planted else 0.0)
     torch.cuda.synchronize()
+    assert bool((out_all[B] == 7.0).all()) and bool((lse_all[B] == 7.0).all())
     for r in range(B):
         kr, vr = pool.read(r, range(n0 + 4))
         kr, vr = kr.double().cpu().numpy()[:, 0], vr.double().cpu().numpy()[:, 0]

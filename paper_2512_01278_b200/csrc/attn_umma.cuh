@@ -123,8 +123,13 @@ __device__ __forceinline__ void verify_body(const Params& p, const int h, const 
   const Item it = load_item(p.items, item_idx);
   const int R = it.nq * G;
   const int Nk = it.num_keys();
-  const int kb = crank * p.chunk;
-  const int ke = min(Nk, kb + p.chunk);
+  // the item's key tiles split evenly over the cluster (counts differ by at most one; the
+  // partial last tile goes to the last CTA, which then streams one mostly empty tile more
+  // than its peers instead of a whole chunk's worth of peers waiting for it); at most
+  // p.chunk / TK tiles per CTA as the planner sized them
+  const int kt = (Nk + TK - 1) / TK;
+  const int kb = (crank * kt / C) * TK;
+  const int ke = min(Nk, ((crank + 1) * kt / C) * TK);
   const int nk = max(0, ke - kb);
   const Sched sc((nk + TK - 1) / TK, S);
   const int nt = sc.nt;

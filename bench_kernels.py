@@ -7,9 +7,10 @@ GQA 4/8, d=128 (BASELINE.json configs[4]).
 One launch = one layer of a batch of requests.  Achieved GB/s = algorithmic
 bytes (K/V rows touched, q/o, lse, score accumulator writes)
 / CUDA-event time, averaged over --iters launches after --warmup.  Before every
-timed launch a 256 MB buffer is written (L2 flush, 2x the 126 MB L2), which also
-keeps the GPU busy while the host enqueues the start event and the launch, so
-the event pair brackets the kernel alone (no host launch latency inside it).
+timed launch a 256 MB buffer is written (L2 flush, 2x the 126 MB L2) and a ~100 µs
+device sleep keeps the GPU busy while the host enqueues the start event and the
+launch, so the event pair brackets the kernel alone (no host launch path inside it; the
+numbers did not move against the flush alone).
 Prints one JSON line per shape.
 """
 
@@ -84,7 +85,10 @@ def main():
             evs = []
             for i in range(args.iters):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                flush.zero_()   # L2 flush; the GPU is busy while the host enqueues e0 + launch
+                flush.zero_()   # L2 flush
+                # keep the GPU busy (~100 us) while the host enqueues e0 + the launch, so the
+                # host-side launch path never shows up between the two events
+                torch.cuda._sleep(200_000)
                 e0.record()
                 fn(i % args.layers)
                 e1.record()

@@ -307,6 +307,7 @@ struct LayerLoop {
   void* const* attn_events;
   int32_t flags;
   void* stream;
+  int l0 = 0, l1 = -1;  // layer range to issue ([0, layers) when l1 < 0)
 };
 
 int issue_layers(const LayerLoop& a, cublasHandle_t hd) {
@@ -330,10 +331,11 @@ int issue_layers(const LayerLoop& a, cublasHandle_t hd) {
   const bool use_table = kv->head_dim % 16 == 0 && (qkv_w % 8) == 0 && workspace != nullptr &&
                          workspace_bytes >= table_bytes + 256 && tab0 >= ws0;
   float2* table = nullptr;
+  const int l0 = a.l0, l1 = a.l1 < 0 ? a.layers : a.l1;
   if (use_table) {
     workspace_bytes = (int64_t)(tab0 - ws0);
     table = reinterpret_cast<float2*>(tab0);
-    sd::rope_table(a.row_pos, rows, kv->head_dim, table, s);
+    if (l0 == 0) sd::rope_table(a.row_pos, rows, kv->head_dim, table, s);  // kept for later layer ranges
   }
   // two attention launches (verify + draft) overlap on priority streams unless timed per
   // launch (attn_events) or disabled (flags bit 0)
@@ -347,7 +349,7 @@ int issue_layers(const LayerLoop& a, cublasHandle_t hd) {
   const void* q = a.q;
   void* ctx = a.ctx;
   int rc;
-  for (int l = 0; l < a.layers; ++l) {
+  for (int l = l0; l < l1; ++l) {
     const sd_layer_weights& wl = a.w[l];
     if ((rc = sd_rmsnorm_cast(x, rows, hidden, a.eps, a.hn, SD_DTYPE_BF16, stream)) != 0) return rc;
     if ((rc = sd::gemm(hd, rows, qkv_w, hidden, a.hn, wl.w_qkv, a.qkv, false, 0.f)) != 0) return rc;
@@ -399,7 +401,7 @@ int issue_layers(const LayerLoop& a, cublasHandle_t hd) {
     if ((rc = sd::gemm(hd, rows, hidden, 2 * hidden, a.hm, wl.mlp_out, x, true, 1.f)) != 0) return rc;
   }
   // the workspace is handed back zero-filled (the attention launches rely on it)
-  if (use_table) cudaMemsetAsync(table, 0, table_bytes, s);
+  if (use_table && l1 == a.layers) cudaMemsetAsync(table, 0, table_bytes, s);
   return 0;
 }
 
@@ -411,10 +413,11 @@ int issue_layers(const LayerLoop& a, cublasHandle_t hd) {
 // touches the one the previous, possibly still running, iteration launched.  The host
 // cost is the capture (~ the eager enqueue) + the update; the device runs the ~300
 // launches without per-launch front-end gaps.
+constexpr int kGraphChunks = 3;
 struct GraphCache {
-  cudaGraphExec_t exec[2] = {nullptr, nullptr};
-  std::vector<unsigned> sig[2];  // cluster shape of every kernel node of the executable
-  int next = 0;
+  cudaGraphExec_t exec[kGraphChunks][2] = {};
+  std::vector<unsigned> sig[kGraphChunks][2];  // cluster shape of every kernel node of the executable
+  int next[kGraphChunks] = {};
   int64_t instantiations = 0, updates = 0;
   // captured and launched on an own stream (the caller's may be the legacy default stream,
   // which cannot be captured), ordered after / before the caller's work by events
@@ -429,45 +432,18 @@ GraphCache* graph_cache() {
   return &gc[dev];
 }
 
-// 0: launched as a graph; 1: capture not possible (caller runs the loop eagerly); < 0 error
-int launch_as_graph(const LayerLoop& a, cublasHandle_t hd) {
-  GraphCache* gc = graph_cache();
-  if (gc == nullptr) return 1;
-  if (gc->cs == nullptr) {
-    if (cudaStreamCreateWithFlags(&gc->cs, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&gc->in, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&gc->out, cudaEventDisableTiming) != cudaSuccess) {
-      cudaGetLastError();
-      gc->cs = nullptr;
-      return 1;
-    }
-  }
-  cudaStream_t caller = static_cast<cudaStream_t>(a.stream);
-  cudaStream_t s = gc->cs;
-  LayerLoop ac = a;
-  ac.stream = s;
-  // every cuBLASLt plan this forward needs is tuned before the capture (tuning synchronises)
-  const int qkv_w = (a.q_heads + 2 * a.kv->kv_heads) * a.kv->head_dim;
-  sd::gemm_prepare(hd, a.rows, qkv_w, a.hidden, false, 0.f);
-  sd::gemm_prepare(hd, a.rows, a.hidden, a.hidden, true, 1.f);
-  sd::gemm_prepare(hd, a.rows, 2 * a.hidden, a.hidden, false, 0.f);
-  sd::gemm_prepare(hd, a.rows, a.hidden, 2 * a.hidden, true, 1.f);
-  if (sd::attn_streams() == nullptr) return 1;
-  cudaGetLastError();
-  // the capture stream waits for the caller's prior work (outside the capture)
-  cudaEventRecord(gc->in, caller);
-  cudaStreamWaitEvent(s, gc->in, 0);
-  cublasSetStream(hd, s);
+// Capture one layer range on the graph stream s, apply it to chunk `ci`'s cached executable
+// and launch it.  0: launched; 1: not capturable (nothing of it ran); < 0: error.
+int capture_chunk(GraphCache* gc, int ci, const LayerLoop& ac, cublasHandle_t hd) {
+  cudaStream_t s = static_cast<cudaStream_t>(ac.stream);
   if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
     cudaGetLastError();
-    cublasSetStream(hd, caller);
     return 1;
   }
   const int64_t launches0 = sd_launch_count();
   const int rc = issue_layers(ac, hd);
   cudaGraph_t g = nullptr;
   const cudaError_t ce = cudaStreamEndCapture(s, &g);
-  cublasSetStream(hd, caller);
   if (rc != 0 || ce != cudaSuccess || g == nullptr) {
     if (g) cudaGraphDestroy(g);
     cudaGetLastError();
@@ -501,10 +477,10 @@ int launch_as_graph(const LayerLoop& a, cublasHandle_t hd) {
     const char* v = getenv("SD_GRAPH_UPDATE");
     return v && *v ? atoi(v) : 1;
   }();
-  const int slot = gc->next;
-  cudaGraphExec_t& ex = gc->exec[slot];
-  gc->next ^= 1;
-  if (ex != nullptr && (!allow_update || gc->sig[slot] != sig)) {
+  const int slot = gc->next[ci];
+  cudaGraphExec_t& ex = gc->exec[ci][slot];
+  gc->next[ci] ^= 1;
+  if (ex != nullptr && (!allow_update || gc->sig[ci][slot] != sig)) {
     cudaGraphExecDestroy(ex);
     ex = nullptr;
   }
@@ -523,18 +499,76 @@ int launch_as_graph(const LayerLoop& a, cublasHandle_t hd) {
       cudaGetLastError();
       ex = nullptr;
       cudaGraphDestroy(g);
-      sd::count_launch(-(int)(sd_launch_count() - launches0));  // nothing of the capture ran
+      sd::count_launch(-(int)(sd_launch_count() - launches0));
       return 1;
     }
     ++gc->instantiations;
-    gc->sig[slot] = std::move(sig);
+    gc->sig[ci][slot] = std::move(sig);
   }
   cudaGraphDestroy(g);
   if (cudaGraphLaunch(ex, s) != cudaSuccess) {
     sd::set_error("sd_forward_layers: cudaGraphLaunch failed");
     return -1;
   }
-  // the caller's later work waits for the graph
+  return 0;
+}
+
+// The layer stack as CUDA graphs of three layer ranges, [0, 2), [2, 8), [8, L): the first
+// range's capture is short, so after an idle stream (the first iteration of a pipeline)
+// the GPU starts within ~0.1 ms while the host captures the rest, instead of waiting for
+// the whole ~2 ms capture.  0: launched; 1: nothing launched (caller issues directly); < 0 error
+int launch_as_graph(const LayerLoop& a, cublasHandle_t hd) {
+  GraphCache* gc = graph_cache();
+  if (gc == nullptr) return 1;
+  if (gc->cs == nullptr) {
+    if (cudaStreamCreateWithFlags(&gc->cs, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&gc->in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&gc->out, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      gc->cs = nullptr;
+      return 1;
+    }
+  }
+  cudaStream_t caller = static_cast<cudaStream_t>(a.stream);
+  cudaStream_t s = gc->cs;
+  // every cuBLASLt plan this forward needs is tuned before the capture (tuning synchronises)
+  const int qkv_w = (a.q_heads + 2 * a.kv->kv_heads) * a.kv->head_dim;
+  sd::gemm_prepare(hd, a.rows, qkv_w, a.hidden, false, 0.f);
+  sd::gemm_prepare(hd, a.rows, a.hidden, a.hidden, true, 1.f);
+  sd::gemm_prepare(hd, a.rows, 2 * a.hidden, a.hidden, false, 0.f);
+  sd::gemm_prepare(hd, a.rows, a.hidden, 2 * a.hidden, true, 1.f);
+  if (sd::attn_streams() == nullptr) return 1;
+  cudaGetLastError();
+  static const int chunked = [] {
+    const char* v = getenv("SD_GRAPH_CHUNKS");
+    return v && *v ? atoi(v) : 1;
+  }();
+  const int bounds[kGraphChunks + 1] = {0, chunked ? std::min(2, a.layers) : 0, chunked ? std::min(8, a.layers) : 0,
+                                        a.layers};
+  // the graph stream waits for the caller's prior work (outside the captures)
+  cudaEventRecord(gc->in, caller);
+  cudaStreamWaitEvent(s, gc->in, 0);
+  cublasSetStream(hd, s);
+  int rc = 0;
+  int ci = 0;
+  for (; ci < kGraphChunks && rc == 0; ++ci) {
+    if (bounds[ci] == bounds[ci + 1]) continue;
+    LayerLoop ac = a;
+    ac.stream = s;
+    ac.l0 = bounds[ci], ac.l1 = bounds[ci + 1];
+    rc = capture_chunk(gc, ci, ac, hd);
+    if (rc == 1) {
+      // not capturable: the rest of the stack goes out directly, still on the graph stream
+      LayerLoop ar = a;
+      ar.stream = s;
+      ar.l0 = bounds[ci];
+      rc = issue_layers(ar, hd);
+      break;
+    }
+  }
+  cublasSetStream(hd, caller);
+  if (rc != 0) return rc < 0 ? rc : -1;
+  // the caller's later work waits for the graphs
   cudaEventRecord(gc->out, s);
   cudaStreamWaitEvent(caller, gc->out, 0);
   return 0;

@@ -197,16 +197,18 @@ def test_native_layer_loop_matches_python_loop_bf16(planted):
     assert (kn - kp).abs().max().item() <= 2e-2 * max(1.0, kp.abs().max().item())
 
 
-def test_forward_graph_equals_direct_launches_bf16():
+@pytest.mark.parametrize("layers", [2, 10])
+def test_forward_graph_equals_direct_launches_bf16(layers):
     """The CUDA-graph path of the native layer loop (csrc/forward.cu launch_as_graph: capture,
     in-place update of a cached executable, re-instantiation when a kernel's cluster shape
     changes) gives bitwise the direct launches' results over a sequence of calls whose K2
-    plans differ (contexts 300 / 6000 / 300 / 2500 rows: different cluster sizes)."""
+    plans differ (contexts 300 / 6000 / 300 / 2500 rows: different cluster sizes); with
+    10 layers the stack is captured as three layer ranges (0-2, 2-8, 8-10)."""
     from paper_2512_01278_b200 import _native as N
     from paper_2512_01278_b200.model import AttnLaunch, forward_rows, lm_head, make_items
     from paper_2512_01278_b200.paged import PagedKvPool
 
-    cfg = M.ModelConfig(2, 16, 4, 128, 1024, seed=9)
+    cfg = M.ModelConfig(layers, 16, 4, 128, 1024, seed=9)
     model = M.init_model(cfg, dtype=torch.bfloat16)
     dev = model.device
     lib = N.load_library()
@@ -242,7 +244,8 @@ def test_forward_graph_equals_direct_launches_bf16():
             M.FORWARD_GRAPH = old
         results[graph] = outs
         if graph:
-            assert lib.sd_forward_graph_stats(0) + lib.sd_forward_graph_stats(1) - inst0 - upd0 == 5
+            chunks = 1 if layers <= 2 else 3
+            assert lib.sd_forward_graph_stats(0) + lib.sd_forward_graph_stats(1) - inst0 - upd0 == 5 * chunks
     for (la, aa), (lb, ab) in zip(results[False], results[True]):
         assert torch.equal(la, lb)
         assert torch.equal(aa, ab)

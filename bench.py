@@ -355,7 +355,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                         clocks=first, B=len(ids), ids=ids, ctx=cw)
             if main is None:
                 main = {"emitted": 0, "dev_s": 0.0, "wall_s": 0.0}
-            summed = ("emitted", "dev_s", "wall_s", "verify_launches", "verify_ms_total", "verify_bytes",
+            summed = ("emitted", "dev_s", "wall_s", "launches", "verify_launches", "verify_ms_total", "verify_bytes",
                       "draft_launches", "draft_ms_total", "draft_bytes")
             for key in summed:
                 if key in r:
